@@ -1,0 +1,138 @@
+/*
+ * rodsim_b200.h -- C ABI of the B200-native CoRdE rod step.
+ *
+ * Drop-in boundary for the reference's compiled core (rodsim._core,
+ * pkg/src/rodsim/_core.pyx).  The reference binds the World's numpy arrays
+ * by raw pointer (make_context, _core.pyx:219-403) and steps them in place;
+ * this library does the same from the host's point of view -- the World
+ * arrays are described by plain pointers and sizes, stay authoritative
+ * between epochs, and are mirrored in HBM while a kernel runs.  No torch or
+ * CUDA types appear in the signatures.
+ *
+ * Entry point                      replaces (reference file:line)
+ * -------------------------------  ------------------------------------------
+ * rs_create                        _core.make_context          _core.pyx:219
+ * rs_upload / rs_download          zero-copy pointer binding   _core.pyx:192-216
+ * rs_run_epoch                     step_serial x K / begin_epoch +
+ *                                  run_epoch_worker + epoch_results
+ *                                                              _core.pyx:1058-1139
+ * rs_error_step                    _core.error_step            _core.pyx:1142
+ * rs_step_counter                  _core.step_counter          _core.pyx:1147
+ * rs_update_params                 _core.update_params         _core.pyx:1083
+ * rs_stage_commands                _core.stage_commands        _core.pyx:1151
+ * rs_applied_step_for              _core.applied_step_for      _core.pyx:1181
+ * rs_read_snapshot                 SnapshotBuffer.read         engine.py:113
+ * rs_destroy                       (context GC)
+ * rs_last_error                    exception text of the above
+ *
+ * Error convention: functions return RS_OK (0) or a negative RS_E* code and
+ * leave a message for rs_last_error().  Like the reference, the kernel never
+ * aborts on non-finite forces or zero-length segments: it records the step
+ * (rs_error_step) and the caller raises FloatingPointError (engine.py:328).
+ */
+#ifndef RODSIM_B200_H
+#define RODSIM_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+enum rs_status {
+    RS_OK = 0,
+    RS_E_INVALID = -1,      /* bad argument (ValueError) */
+    RS_E_CUDA = -2,         /* CUDA runtime failure (RuntimeError) */
+    RS_E_UNSUPPORTED = -3,  /* scene feature outside this build's scope */
+    RS_E_RING_FULL = -4     /* command ring full (RuntimeError) */
+};
+
+enum rs_precision {
+    RS_F64_MIRROR = 0,      /* fp64, no FMA, reference rounding: bitwise parity */
+    RS_F32 = 1,             /* fp32 with FMA: tolerance parity */
+    RS_F64_FAST = 2         /* fp64 with FMA: 1e-9 parity on well-conditioned scenes */
+};
+
+/* upload / download masks */
+#define RS_STATE   0x1u     /* positions, velocities, frames, angular velocities */
+#define RS_STATIC  0x2u     /* material arrays, masses, locks, bindings, maps */
+#define RS_CONTROL 0x4u     /* drivers and grab anchors */
+
+/* Host view of a World (world.py:77-182).  All arrays are C-contiguous,
+ * float64 / int64 / uint8 exactly as the reference World holds them, and
+ * must outlive the handle (the reference keeps them alive via ctx.refs). */
+typedef struct rs_world_desc {
+    int32_t abi_version;    /* RS_ABI_VERSION */
+    int32_t precision;      /* enum rs_precision */
+    int32_t device;         /* CUDA device ordinal */
+    int32_t force_tier;     /* -1 auto; 0 CTA, 1 cluster, 2 grid (testing) */
+    int32_t force_ctas;     /* 0 auto; >0 CTAs per rod for cluster/grid tiers */
+    int32_t force_variant;  /* -1 auto; else CTA-tier variant index (testing) */
+    int64_t P, E, R;        /* points, elements, rods */
+    int64_t iters;          /* solver.iterations */
+    int64_t step_index;     /* world.step_index: initial core step counter */
+    double dt, beta, gx, gy, gz;
+    const int64_t *rod_offsets;       /* (R+1) first point of each rod, P */
+    /* dynamic state (rs_upload RS_STATE / rs_download RS_STATE) */
+    double *pos, *vel, *q, *w;        /* (P,3) (P,3) (E,4) (E,3) */
+    /* constants (RS_STATIC) */
+    const double *rest, *ustar, *mass, *invm, *inert, *fext;
+    const double *ks, *kp, *gt, *gr, *ext, *kb;
+    const uint8_t *plock, *flock, *jvalid;
+    const int64_t *elem_point, *elem_parity;
+    const int64_t *drv_pt, *drv_fr;   /* (R) driven point / frame or -1 */
+    int64_t nbind;
+    const int64_t *bind_a, *bind_b, *bind_mode;
+    /* control (RS_CONTROL); also mutated by staged commands */
+    double *drv_v, *drv_rot;          /* (R,3) (R) */
+    int64_t ngrab;
+    uint8_t *g_act;
+    int64_t *g_pt;
+    double *g_tgt;                    /* (ngrab,3) */
+} rs_world_desc;
+
+typedef struct rs_handle_s *rs_handle;
+
+int rs_create(const rs_world_desc *desc, rs_handle *out);
+int rs_upload(rs_handle h, uint32_t mask);
+/* Advance `steps` time steps on the device state (K steps per launch).
+ * Applies commands staged with rs_stage_commands at the first step boundary.
+ * contacts: always 0 in this build (no mesh / self-collision); barrier_ns:
+ * 0 (barriers are on-chip).  Either pointer may be NULL. */
+int rs_run_epoch(rs_handle h, int64_t steps, int64_t *contacts, int64_t *barrier_ns);
+int rs_download(rs_handle h, uint32_t mask);
+int rs_synchronize(rs_handle h);
+int64_t rs_error_step(rs_handle h);
+int64_t rs_step_counter(rs_handle h);
+int rs_update_params(rs_handle h, double dt, int64_t iters);
+/* ops: (n,6) rows [op, i0, i1, f0, f1, f2], ops 0..3 = driver velocity,
+ * driver rotation, grab, release (engine.py:30-34). slots: (n) out. */
+int rs_stage_commands(rs_handle h, const double *ops, int64_t n, int64_t *slots);
+int64_t rs_applied_step_for(rs_handle h, int64_t global_slot);
+/* Snapshot of the last completed epoch: pos (P,3), q (E,4). */
+int rs_read_snapshot(rs_handle h, double *pos, double *q, int64_t *seq, int64_t *step);
+void rs_destroy(rs_handle h);
+const char *rs_last_error(void);
+
+/* Measurement helpers (bench / tests). */
+/* Time the kernels of the last rs_run_epoch with CUDA events on the
+ * launching stream; returns milliseconds of the last epoch's launches. */
+int rs_enable_timing(rs_handle h, int on);
+double rs_last_kernel_ms(rs_handle h);
+/* Number of kernel launches issued so far. */
+int64_t rs_launch_count(rs_handle h);
+/* JSON description of the launch plan (tiers, CTAs, threads, variants). */
+int rs_plan_json(rs_handle h, char *buf, int64_t len);
+/* Raw device pointer of a state array: 0 pos, 1 vel, 2 q, 3 w (element
+ * type double for RS_F64_*, float for RS_F32). */
+int rs_device_ptr(rs_handle h, int32_t which, void **out);
+/* Self-test: IEEE a/b and the kernel's reciprocal-based quotient for n
+ * pairs, computed on the device with the fp64 mirror build flags. */
+int rs_selftest_div(const double *a, const double *b, int64_t n, double *q_ieee,
+                    double *q_fast);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

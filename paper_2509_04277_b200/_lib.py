@@ -1,0 +1,274 @@
+"""ctypes binding of the C ABI in include/rodsim_b200.h.
+
+`librodsim_b200.so` is built in-tree (`make`, or `__graft_entry__.build()`)
+and holds the sm_100a kernels.  There is no fallback: importing the engine
+without the library, or running it without a CUDA device, raises.
+"""
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        "librodsim_b200.so")
+
+RS_ABI_VERSION = 1
+RS_OK = 0
+RS_E_INVALID = -1
+RS_E_CUDA = -2
+RS_E_UNSUPPORTED = -3
+RS_E_RING_FULL = -4
+
+RS_F64_MIRROR = 0
+RS_F32 = 1
+RS_F64_FAST = 2
+PRECISIONS = {"f64": RS_F64_MIRROR, "f32": RS_F32, "f64_fast": RS_F64_FAST}
+
+RS_STATE = 0x1
+RS_STATIC = 0x2
+RS_CONTROL = 0x4
+
+_p = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_f64 = ctypes.c_double
+
+
+class WorldDesc(ctypes.Structure):
+    """Mirror of `rs_world_desc`."""
+
+    _fields_ = [
+        ("abi_version", _i32), ("precision", _i32), ("device", _i32),
+        ("force_tier", _i32), ("force_ctas", _i32), ("force_variant", _i32),
+        ("P", _i64), ("E", _i64), ("R", _i64), ("iters", _i64),
+        ("step_index", _i64),
+        ("dt", _f64), ("beta", _f64), ("gx", _f64), ("gy", _f64), ("gz", _f64),
+        ("rod_offsets", _p),
+        ("pos", _p), ("vel", _p), ("q", _p), ("w", _p),
+        ("rest", _p), ("ustar", _p), ("mass", _p), ("invm", _p),
+        ("inert", _p), ("fext", _p),
+        ("ks", _p), ("kp", _p), ("gt", _p), ("gr", _p), ("ext", _p),
+        ("kb", _p),
+        ("plock", _p), ("flock", _p), ("jvalid", _p),
+        ("elem_point", _p), ("elem_parity", _p),
+        ("drv_pt", _p), ("drv_fr", _p),
+        ("nbind", _i64), ("bind_a", _p), ("bind_b", _p), ("bind_mode", _p),
+        ("drv_v", _p), ("drv_rot", _p),
+        ("ngrab", _i64), ("g_act", _p), ("g_pt", _p), ("g_tgt", _p),
+    ]
+
+
+# (symbol, restype, argtypes) of every entry point declared in the header
+SIGNATURES = [
+    ("rs_create", _i32, [ctypes.POINTER(WorldDesc), ctypes.POINTER(_p)]),
+    ("rs_upload", _i32, [_p, ctypes.c_uint32]),
+    ("rs_run_epoch", _i32, [_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    ("rs_download", _i32, [_p, ctypes.c_uint32]),
+    ("rs_synchronize", _i32, [_p]),
+    ("rs_error_step", _i64, [_p]),
+    ("rs_step_counter", _i64, [_p]),
+    ("rs_update_params", _i32, [_p, _f64, _i64]),
+    ("rs_stage_commands", _i32, [_p, _p, _i64, _p]),
+    ("rs_applied_step_for", _i64, [_p, _i64]),
+    ("rs_read_snapshot", _i32, [_p, _p, _p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    ("rs_destroy", None, [_p]),
+    ("rs_last_error", ctypes.c_char_p, []),
+    ("rs_enable_timing", _i32, [_p, _i32]),
+    ("rs_last_kernel_ms", _f64, [_p]),
+    ("rs_launch_count", _i64, [_p]),
+    ("rs_plan_json", _i32, [_p, ctypes.c_char_p, _i64]),
+    ("rs_device_ptr", _i32, [_p, _i32, ctypes.POINTER(_p)]),
+    ("rs_selftest_div", _i32, [_p, _p, _i64, _p, _p]),
+]
+
+_LIB = None
+
+
+def load_library(path=None):
+    """Load (once) and type the shared library; raises if it is missing."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not found: build the CUDA library first "
+            "(`make` or `python -c 'import __graft_entry__ as g; g.build()'`)")
+    lib = ctypes.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path == LIB_PATH:
+        _LIB = lib
+    return lib
+
+
+class RodsimError(RuntimeError):
+    pass
+
+
+def check(code, lib=None):
+    if code == RS_OK:
+        return
+    lib = lib or load_library()
+    msg = lib.rs_last_error().decode(errors="replace")
+    if code == RS_E_INVALID:
+        raise ValueError(msg)
+    if code == RS_E_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RodsimError(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class DeviceWorld:
+    """One device mirror of a World (a C handle) plus the arrays it binds.
+
+    `arrays` keeps every bound numpy array alive, like the reference
+    context's `refs` (_core.pyx:180, 402).
+    """
+
+    def __init__(self, world, precision="f64", device=0, force_tier=-1,
+                 force_ctas=0, force_variant=-1):
+        self.lib = load_library()
+        self.world = world
+        self.precision = precision
+        w = world
+        c = np.ascontiguousarray
+        offs = np.array([i.point_offset for i in w.rod_infos]
+                        + [w.num_points], dtype=np.int64)
+        self.arrays = {
+            "rod_offsets": offs,
+            "pos": w.positions, "vel": w.velocities, "q": w.frames,
+            "w": w.angular_velocities,
+            "rest": c(w.rest_lengths), "ustar": c(w.intrinsic_strains),
+            "mass": c(w.masses), "invm": c(w.inv_masses),
+            "inert": c(w.inertias), "fext": c(w.external_forces),
+            "ks": c(w.stretch_k), "kp": c(w.penalty_k), "gt": c(w.gamma_t),
+            "gr": c(w.gamma_r), "ext": c(w.extensible), "kb": c(w.bend_k),
+            "plock": c(w.point_locked).view(np.uint8),
+            "flock": c(w.frame_locked).view(np.uint8),
+            "jvalid": c(w.junction_valid).view(np.uint8),
+            "elem_point": c(w.elem_point, dtype=np.int64),
+            "elem_parity": c(w.elem_parity, dtype=np.int64),
+            "drv_pt": c(w.driven_point, dtype=np.int64),
+            "drv_fr": c(w.driven_frame, dtype=np.int64),
+            "bind_a": c(w.bind_a, dtype=np.int64),
+            "bind_b": c(w.bind_b, dtype=np.int64),
+            "bind_mode": c(w.bind_mode, dtype=np.int64),
+            "drv_v": w.driver_velocity, "drv_rot": w.driver_rotation,
+            "g_act": w.grab_active, "g_pt": w.grab_point,
+            "g_tgt": w.grab_target,
+        }
+        for k in ("pos", "vel", "q", "w", "drv_v", "drv_rot", "g_act",
+                  "g_pt", "g_tgt"):
+            a = self.arrays[k]
+            if not (a.flags.c_contiguous and a.flags.writeable):
+                raise ValueError(f"world array {k} must be C-contiguous and writeable")
+        d = WorldDesc()
+        d.abi_version = RS_ABI_VERSION
+        d.precision = PRECISIONS[precision]
+        d.device = device
+        d.force_tier = force_tier
+        d.force_ctas = force_ctas
+        d.force_variant = force_variant
+        d.P, d.E, d.R = w.num_points, w.num_elements, len(w.rod_infos)
+        d.iters = w.solver.iterations
+        d.step_index = w.step_index
+        d.dt = w.dt
+        d.beta = w.solver.position_bias
+        d.gx, d.gy, d.gz = (float(x) for x in w.gravity)
+        for name, arr in self.arrays.items():
+            setattr(d, name, _ptr(arr))
+        d.nbind = self.arrays["bind_a"].shape[0]
+        d.ngrab = self.arrays["g_act"].shape[0]
+        self.desc = d
+        h = _p()
+        check(self.lib.rs_create(ctypes.byref(d), ctypes.byref(h)), self.lib)
+        self.handle = h
+
+    def state_pointers(self):
+        return tuple(self.arrays[k].ctypes.data for k in ("pos", "vel", "q", "w"))
+
+    def upload(self, mask):
+        check(self.lib.rs_upload(self.handle, mask), self.lib)
+
+    def run(self, steps):
+        contacts, bns = _i64(0), _i64(0)
+        check(self.lib.rs_run_epoch(self.handle, int(steps), ctypes.byref(contacts),
+                                    ctypes.byref(bns)), self.lib)
+        return contacts.value, bns.value
+
+    def download(self, mask=RS_STATE):
+        check(self.lib.rs_download(self.handle, mask), self.lib)
+
+    def synchronize(self):
+        check(self.lib.rs_synchronize(self.handle), self.lib)
+
+    def error_step(self):
+        return int(self.lib.rs_error_step(self.handle))
+
+    def step_counter(self):
+        return int(self.lib.rs_step_counter(self.handle))
+
+    def update_params(self, dt, iters):
+        check(self.lib.rs_update_params(self.handle, float(dt), int(iters)), self.lib)
+
+    def stage_commands(self, ops):
+        ops = np.ascontiguousarray(ops, dtype=np.float64)
+        if ops.ndim != 2 or ops.shape[1] != 6:
+            raise ValueError("ops must have shape (n, 6)")
+        slots = np.zeros(ops.shape[0], dtype=np.int64)
+        code = self.lib.rs_stage_commands(self.handle, ops.ctypes.data, ops.shape[0],
+                                          slots.ctypes.data)
+        if code == RS_E_RING_FULL:
+            raise RuntimeError(self.lib.rs_last_error().decode())
+        check(code, self.lib)
+        return [int(s) for s in slots]
+
+    def applied_step_for(self, slot):
+        return int(self.lib.rs_applied_step_for(self.handle, int(slot)))
+
+    def read_snapshot(self):
+        w = self.world
+        pos = np.empty((w.num_points, 3))
+        q = np.empty((w.num_elements, 4))
+        seq, step = _i64(0), _i64(0)
+        check(self.lib.rs_read_snapshot(self.handle, pos.ctypes.data, q.ctypes.data,
+                                        ctypes.byref(seq), ctypes.byref(step)), self.lib)
+        return seq.value, step.value, pos, q
+
+    def enable_timing(self, on=True):
+        check(self.lib.rs_enable_timing(self.handle, 1 if on else 0), self.lib)
+
+    def last_kernel_ms(self):
+        return float(self.lib.rs_last_kernel_ms(self.handle))
+
+    def launch_count(self):
+        return int(self.lib.rs_launch_count(self.handle))
+
+    def plan(self):
+        buf = ctypes.create_string_buffer(1 << 16)
+        check(self.lib.rs_plan_json(self.handle, buf, len(buf)), self.lib)
+        return json.loads(buf.value.decode())
+
+    def device_ptr(self, which):
+        out = _p()
+        check(self.lib.rs_device_ptr(self.handle, int(which), ctypes.byref(out)), self.lib)
+        return out.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.rs_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,109 @@
+// rod_common.h -- structures shared by the host planner (rodsim_capi.cu) and
+// the sm_100a step kernels (rod_step.cuh).
+//
+// Vocabulary: a rod has P_r mass points and E_r = P_r - 1
+// elements; element j spans points j, j+1 and carries frame j.  On the device
+// a *slot* is one point of a CTA's contiguous point range together with the
+// element whose lower point it is (absent for the last point of a rod).
+#pragma once
+#include <stdint.h>
+
+namespace rsb {
+
+// per-point flags (uint32), built on the host from the World arrays
+enum SlotFlag : uint32_t {
+    SF_HAS_ELEM = 1u << 0,   // point is not the last of its rod: element e exists
+    SF_HAS_PREV = 1u << 1,   // point is not the first of its rod (pt_ehi >= 0)
+    SF_JVALID   = 1u << 2,   // junction e|e+1 valid (world.junction_valid[e])
+    SF_JPREV    = 1u << 3,   // junction e-1|e valid
+    SF_PLOCK    = 1u << 4,   // world.point_locked[p]
+    SF_FLOCK    = 1u << 5,   // world.frame_locked[e]
+    SF_EXT      = 1u << 6,   // world.extensible[e] != 0
+    SF_PARITY   = 1u << 7,   // world.elem_parity[e] & 1
+    SF_DRV_PT   = 1u << 8,   // point velocity overwritten by a driver
+    SF_DRV_FR   = 1u << 9,   // frame angular velocity overwritten by a driver
+    SF_DIST     = 1u << 10,  // element takes part in the distance projection
+    // bits 16..23 / 24..31: index into the CTA's driver table for the point
+    // (DRV_PT) and the frame (DRV_FR) driver of this slot
+};
+constexpr int SF_DRV_PT_SHIFT = 16;
+constexpr int SF_DRV_FR_SHIFT = 24;
+constexpr int MAX_DRV_PER_CTA = 255;
+
+// One CTA's share of the world: a contiguous point range [p0, p0+np).
+struct CtaTask {
+    int32_t p0;          // first global point
+    int32_t np;          // number of points (slots) owned
+    int32_t bind_begin;  // range in the binding table
+    int32_t bind_count;
+    int32_t grab_begin;  // range in the per-epoch grab table
+    int32_t grab_count;
+    int32_t drv_begin;   // range in the driver table
+    int32_t drv_count;
+    int32_t bind_seq;    // 1: bindings overlap (not a matching) -> ordered
+    int32_t e_uni;       // element whose constants stand for the whole CTA
+                         // when the launch uses CTA-uniform constants
+    int32_t pad[2];
+};
+
+// A binding endpoint pair resolved to (cta rank within the cluster, slot).
+struct BindEntry {
+    int32_t a_rank, a_slot;
+    int32_t b_rank, b_slot;
+    int32_t mode;        // 0 one-way (a dominates), 1 bidirectional
+    int32_t pad;
+};
+
+struct GrabEntry {
+    int32_t slot;        // local slot of the grabbed point
+    int32_t world_slot;  // grab slot index in the World (ordering key)
+    double tgt[3];
+};
+
+struct DrvEntry {
+    int32_t slot;        // local slot
+    int32_t kind;        // 0 point velocity, 1 frame rotation
+    int32_t rod;         // row of world.driver_velocity / driver_rotation
+    int32_t pad;
+};
+
+enum Tier : int { TIER_CTA = 0, TIER_CLUSTER = 1, TIER_GRID = 2 };
+
+// Kernel arguments; device pointers, AoS layouts identical to world.py.
+template <typename Real>
+struct StepArgs {
+    Real *pos, *vel, *q, *w;                       // (P,3) (P,3) (E,4) (E,3)
+    const Real *rest, *ustar, *inert, *ks, *kp, *gt, *gr, *kb;  // per element
+    const Real *mass, *invm, *fext;                // per point
+    const Real *drv_v, *drv_rot;                   // (R,3), (R)
+    const uint32_t *pflags;                        // (P)
+    const int32_t *pt_elem;                        // (P) element or -1
+    const CtaTask *tasks;
+    const BindEntry *binds;
+    const GrabEntry *grabs;
+    const DrvEntry *drvs;
+    // grid tier: neighbour flags and double-buffered boundary halos
+    int32_t *flags;                                // (ncta)
+    Real *halo;                                    // (2, ncta, HALO_WORDS)
+    unsigned long long *err_step;                  // max erroring step + 1 (0 = none)
+    int64_t step0;                                 // core step counter at launch
+    int32_t steps;                                 // K steps per launch
+    int32_t iters;
+    int32_t bind_cap;                              // smem binding slots per CTA
+    int32_t drv_cap;                               // smem driver slots per CTA
+    int32_t has_fext;
+    int32_t ncta;
+    int32_t debug;                                 // bit 0: poison smem (NaN) first
+    Real dt, beta, gx, gy, gz;
+};
+
+// grid-tier halo record per CTA and buffer (Real words)
+constexpr int HALO_WORDS = 32;
+// layout inside a halo record
+enum HaloOff : int {
+    H_FIRST_POS = 0, H_FIRST_VEL = 3, H_FIRST_Q = 6, H_FIRST_W = 10,   // slot 0
+    H_LAST_POS = 13, H_LAST_VEL = 16,                                    // last slot
+    H_LAST_EF = 19, H_LAST_FN = 22, H_LAST_JT = 26,                      // last slot
+};
+
+}  // namespace rsb

@@ -1,0 +1,133 @@
+// rod_launch.cuh -- instantiation table and launchers for rod_step_kernel.
+// Included by one translation unit per arithmetic mode; RSB_MODE_NS names
+// the mode (mirror: --fmad=false fp64, bit-identical to the reference;
+// fast: contraction allowed, fp32 and fp64).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "rod_step.cuh"
+
+#if !defined(RSB_MODE_NS) || !defined(RSB_MODE_ID)
+#error "define RSB_MODE_NS and RSB_MODE_ID before including rod_launch.cuh"
+#endif
+
+namespace rsb {
+namespace RSB_MODE_NS {
+
+// (slots per thread S, slot capacity per CTA CAP); CAP/S threads is a
+// multiple of 128 so the register budget per thread is 65536/(CAP/S).
+//   V0 (1,128)  V1 (1,256)  V2 (2,512)  V3 (2,768)  V4 (3,1152)
+// Cluster and grid tiers use V2 or V4.
+
+template <typename Real, int S, int CAP, int TIER, bool UNI>
+static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
+                              size_t smem, int cluster, cudaStream_t st) {
+    auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    if constexpr (TIER == TIER_CLUSTER) {
+        if (cluster > 8) {
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ncta);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fn, a);
+    } else if constexpr (TIER == TIER_GRID) {
+        void* args[] = {const_cast<StepArgs<Real>*>(&a)};
+        return cudaLaunchCooperativeKernel((const void*)fn, dim3(ncta), dim3(threads), args, smem, st);
+    } else {
+        fn<<<ncta, threads, smem, st>>>(a);
+        return cudaGetLastError();
+    }
+}
+
+template <typename Real, int S, int CAP, int TIER, bool UNI>
+static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out) {
+    auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    if constexpr (TIER == TIER_CLUSTER) {
+        if (cluster > 8) {
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cluster);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaOccupancyMaxActiveClusters(out, (void*)fn, &cfg);
+    } else {
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, threads, smem);
+    }
+}
+
+// what: 0 = launch, 1 = occupancy query
+template <typename Real, int S, int CAP, int TIER>
+static cudaError_t dispatch_uni(int what, bool uni, const StepArgs<Real>* a, int ncta, int threads,
+                                size_t smem, int cluster, cudaStream_t st, int* out) {
+    if (what == 0)
+        return uni ? launch_one<Real, S, CAP, TIER, true>(*a, ncta, threads, smem, cluster, st)
+                   : launch_one<Real, S, CAP, TIER, false>(*a, ncta, threads, smem, cluster, st);
+    return uni ? occupancy_one<Real, S, CAP, TIER, true>(threads, smem, cluster, out)
+               : occupancy_one<Real, S, CAP, TIER, false>(threads, smem, cluster, out);
+}
+
+template <typename Real>
+static cudaError_t dispatch(int what, int variant, int tier, bool uni, const StepArgs<Real>* a,
+                            int ncta, int threads, size_t smem, int cluster, cudaStream_t st,
+                            int* out) {
+#define RSB_D(S, CAP, TIER) dispatch_uni<Real, S, CAP, TIER>(what, uni, a, ncta, threads, smem, cluster, st, out)
+    if (tier == TIER_CTA) {
+        switch (variant) {
+            case 0: return RSB_D(1, 128, TIER_CTA);
+            case 1: return RSB_D(1, 256, TIER_CTA);
+            case 2: return RSB_D(2, 512, TIER_CTA);
+            case 3: return RSB_D(2, 768, TIER_CTA);
+            case 4: return RSB_D(3, 1152, TIER_CTA);
+        }
+    } else if (tier == TIER_CLUSTER) {
+        switch (variant) {
+            case 2: return RSB_D(2, 512, TIER_CLUSTER);
+            case 4: return RSB_D(3, 1152, TIER_CLUSTER);
+        }
+    } else if (tier == TIER_GRID) {
+        switch (variant) {
+            case 2: return RSB_D(2, 512, TIER_GRID);
+            case 4: return RSB_D(3, 1152, TIER_GRID);
+        }
+    }
+#undef RSB_D
+    return cudaErrorInvalidValue;
+}
+
+template <typename Real>
+cudaError_t launch_step(int variant, int tier, bool uni, const StepArgs<Real>& a, int ncta,
+                        int threads, size_t smem, int cluster, cudaStream_t st) {
+    return dispatch<Real>(0, variant, tier, uni, &a, ncta, threads, smem, cluster, st, nullptr);
+}
+
+template <typename Real>
+cudaError_t occupancy(int variant, int tier, bool uni, int threads, size_t smem, int cluster, int* out) {
+    return dispatch<Real>(1, variant, tier, uni, nullptr, 0, threads, smem, cluster, nullptr, out);
+}
+
+}  // namespace RSB_MODE_NS
+}  // namespace rsb

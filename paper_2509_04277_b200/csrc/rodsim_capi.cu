@@ -1,0 +1,1061 @@
+// rodsim_capi.cu -- host side of the C ABI (include/rodsim_b200.h):
+// device mirrors of the World arrays, the launch planner (CTA / cluster /
+// grid tiers), epoch execution, command ring and snapshot.
+//
+// The planner's job is to map the reference's "block" decomposition
+// (partition.py, _core.pyx:360-377) onto the B200: whole rods are packed into
+// CTAs; a rod (or a set of rods coupled by bindings) too large for one CTA is
+// split across the CTAs of a thread-block cluster; a rod too large for a
+// 16-CTA cluster runs on a cooperative grid.  The oracle is bitwise invariant
+// to the partition, so the mapping is free.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/rodsim_b200.h"
+#include "rod_common.h"
+#include "rod_step.cuh"
+
+namespace rsb {
+namespace mirror {
+template <typename Real>
+cudaError_t launch_step(int, int, bool, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
+template <typename Real>
+cudaError_t occupancy(int, int, bool, int, size_t, int, int*);
+}  // namespace mirror
+namespace fast {
+template <typename Real>
+cudaError_t launch_step(int, int, bool, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
+template <typename Real>
+cudaError_t occupancy(int, int, bool, int, size_t, int, int*);
+}  // namespace fast
+}  // namespace rsb
+
+using namespace rsb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                       \
+    do {                                                                            \
+        cudaError_t e_ = (x);                                                       \
+        if (e_ != cudaSuccess)                                                      \
+            return fail(RS_E_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                        \
+    } while (0)
+
+struct Variant {
+    int S, CAP;
+};
+constexpr Variant kVariants[] = {{1, 128}, {1, 256}, {2, 512}, {2, 768}, {3, 1152}};
+constexpr int kNumVariants = 5;
+constexpr int kClusterVariant = 4;
+constexpr int kMaxCluster = 16;
+constexpr int kRingCap = 64;
+constexpr int kMaxStepsPerLaunch = 1 << 16;
+constexpr size_t kMaxSmem = 232448;   // 227 KB opt-in per CTA on sm_100
+
+struct Segment {     // consecutive rods that must share a CTA / cluster / grid
+    int r0, r1;      // rods [r0, r1]
+    int64_t p0, p1;  // points [p0, p1)
+};
+
+struct Group {       // one kernel launch
+    int tier = TIER_CTA;
+    int variant = 0;
+    bool uni = false;
+    int task_begin = 0, ncta = 0;
+    int threads = 0;
+    int cluster = 1;
+    int bind_cap = 0, drv_cap = 0;
+    size_t smem = 0;
+    int32_t* d_flags = nullptr;   // grid tier
+    void* d_halo = nullptr;
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct rs_handle_s {
+    rs_world_desc d{};
+    int prec = RS_F64_MIRROR;
+    size_t rsz = 8;                 // sizeof(Real) on the device
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timing = false;
+    bool timed = false;
+    double last_ms = 0.0;
+    int64_t launches = 0;
+    int num_sms = 0;
+    int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
+
+    // device mirrors
+    DevBuf pos, vel, q, w;
+    DevBuf rest, ustar, inert, ks, kp, gt, gr, kb, mass, invm, fext, drv_v, drv_rot;
+    DevBuf pflags, pt_elem, tasks, binds, drvs, grabs;
+    unsigned long long* d_err = nullptr;
+    unsigned long long* h_err = nullptr;   // pinned
+    int has_fext = 0;
+
+    // plan
+    std::vector<CtaTask> h_tasks;
+    std::vector<BindEntry> h_binds;
+    std::vector<DrvEntry> h_drvs;
+    std::vector<GrabEntry> h_grabs;
+    std::vector<Group> groups;
+    std::vector<int64_t> task_p0_sorted;   // (p0, task) lookup for grabs
+    std::vector<int> task_by_p0;
+    std::vector<int> task_group;
+    bool planned = false;
+
+    // counters, ring, snapshot
+    int64_t step = 0;
+    int64_t err_step = -1;
+    std::mutex ring_mu;
+    double ring[kRingCap][6];
+    int64_t ring_apply[kRingCap];
+    int64_t head = 0, tail = 0;
+    bool control_dirty = false;
+    int64_t snap_seq = 0, snap_step = 0;
+
+    // host staging (pinned) for precision conversion
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+    std::vector<void*> registered;
+};
+
+namespace {
+
+int dev_alloc(DevBuf& b, size_t bytes) {
+    if (b.bytes >= bytes && b.p) return RS_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    if (bytes == 0) return RS_OK;
+    CK(cudaMalloc(&b.p, bytes));
+    b.bytes = bytes;
+    return RS_OK;
+}
+
+int ensure_stage(rs_handle h, size_t bytes) {
+    if (h->stage_bytes >= bytes) return RS_OK;
+    if (h->stage) {
+        cudaStreamSynchronize(h->st);
+        cudaFreeHost(h->stage);
+    }
+    h->stage = nullptr;
+    h->stage_bytes = 0;
+    CK(cudaMallocHost(&h->stage, bytes));
+    h->stage_bytes = bytes;
+    return RS_OK;
+}
+
+// host double array -> device Real array
+int put_real(rs_handle h, DevBuf& b, const double* src, size_t count) {
+    int rc = dev_alloc(b, std::max<size_t>(count, 1) * h->rsz);
+    if (rc) return rc;
+    if (count == 0 || !src) return RS_OK;
+    if (h->rsz == sizeof(double)) {
+        CK(cudaMemcpyAsync(b.p, src, count * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    } else {
+        rc = ensure_stage(h, count * sizeof(float));
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(h->st));   // staging buffer reuse
+        float* s = static_cast<float*>(h->stage);
+        for (size_t i = 0; i < count; ++i) s[i] = float(src[i]);
+        CK(cudaMemcpyAsync(b.p, s, count * sizeof(float), cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    return RS_OK;
+}
+
+// device Real array -> host double array (synchronous for fp32)
+int get_real(rs_handle h, const DevBuf& b, double* dst, size_t count) {
+    if (count == 0 || !dst) return RS_OK;
+    if (h->rsz == sizeof(double)) {
+        CK(cudaMemcpyAsync(dst, b.p, count * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    } else {
+        int rc = ensure_stage(h, count * sizeof(float));
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(h->stage, b.p, count * sizeof(float), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        const float* s = static_cast<const float*>(h->stage);
+        for (size_t i = 0; i < count; ++i) dst[i] = double(s[i]);
+    }
+    return RS_OK;
+}
+
+template <typename T>
+int put_vec(rs_handle h, DevBuf& b, const std::vector<T>& v) {
+    int rc = dev_alloc(b, std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (rc) return rc;
+    if (!v.empty()) CK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->st));
+    // the vectors may be rebuilt before the copy runs
+    CK(cudaStreamSynchronize(h->st));
+    return RS_OK;
+}
+
+int64_t rod_of(const rs_world_desc& d, int64_t p) {
+    const int64_t* o = d.rod_offsets;
+    return int64_t(std::upper_bound(o, o + d.R + 1, p) - o) - 1;
+}
+
+// ---- launch planning --------------------------------------------------------
+
+int occupancy_query(rs_handle h, int variant, int tier, bool uni, int threads, size_t smem,
+                    int cluster, int* out) {
+    cudaError_t e;
+    if (h->prec == RS_F64_MIRROR)
+        e = mirror::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
+    else if (h->prec == RS_F32)
+        e = fast::occupancy<float>(variant, tier, uni, threads, smem, cluster, out);
+    else
+        e = fast::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
+    if (e != cudaSuccess)
+        return fail(RS_E_CUDA, "occupancy query failed: %s", cudaGetErrorString(e));
+    return RS_OK;
+}
+
+bool elem_consts_equal(const rs_world_desc& d, int64_t a, int64_t b) {
+    auto eq = [](double x, double y) { return std::memcmp(&x, &y, sizeof x) == 0; };
+    if (!eq(d.rest[a], d.rest[b]) || !eq(d.ks[a], d.ks[b]) || !eq(d.kp[a], d.kp[b]) ||
+        !eq(d.gt[a], d.gt[b]) || !eq(d.gr[a], d.gr[b]))
+        return false;
+    for (int k = 0; k < 3; ++k)
+        if (!eq(d.kb[3 * a + k], d.kb[3 * b + k]) || !eq(d.ustar[3 * a + k], d.ustar[3 * b + k]) ||
+            !eq(d.inert[3 * a + k], d.inert[3 * b + k]))
+            return false;
+    return true;
+}
+
+int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_elem) {
+    const rs_world_desc& d = h->d;
+    const int64_t P = d.P, R = d.R;
+    if (P >= (int64_t(1) << 31)) return fail(RS_E_INVALID, "too many points for int32 indexing");
+
+    // -- per-point flags and element map (validates the flat layout) ------
+    pflags.assign(P, 0u);
+    pt_elem.assign(P, -1);
+    for (int64_t r = 0; r < R; ++r) {
+        const int64_t o = d.rod_offsets[r], np = d.rod_offsets[r + 1] - o;
+        if (np < 2) return fail(RS_E_INVALID, "rod %lld has fewer than two points", (long long)r);
+        for (int64_t i = 0; i < np; ++i) {
+            const int64_t p = o + i;
+            uint32_t f = 0;
+            if (d.plock[p]) f |= SF_PLOCK;
+            if (i > 0) f |= SF_HAS_PREV;
+            if (i < np - 1) {
+                const int64_t e = p - r;
+                f |= SF_HAS_ELEM;
+                pt_elem[p] = int32_t(e);
+                if (d.elem_point[e] != p)
+                    return fail(RS_E_INVALID, "elem_point[%lld] != %lld: non-standard layout",
+                                (long long)e, (long long)p);
+                if (d.jvalid[e]) {
+                    if (i >= np - 2)
+                        return fail(RS_E_INVALID, "junction_valid[%lld] set at a rod end", (long long)e);
+                    f |= SF_JVALID;
+                }
+                if (e > 0 && d.jvalid[e - 1]) {
+                    if (i == 0)
+                        return fail(RS_E_INVALID, "junction_valid[%lld] crosses rods", (long long)(e - 1));
+                    f |= SF_JPREV;
+                }
+                if (d.flock[e]) f |= SF_FLOCK;
+                if (d.ext[e] != 0.0) f |= SF_EXT;
+                else f |= SF_DIST;
+                const int64_t par = d.elem_parity[e];
+                if (par != 0 && par != 1)
+                    return fail(RS_E_INVALID, "elem_parity[%lld] must be 0 or 1", (long long)e);
+                if (par) f |= SF_PARITY;
+            }
+            pflags[p] = f;
+        }
+    }
+
+    // -- segments: rods coupled by bindings must share a CTA / cluster ------
+    std::vector<int> lo(R), hi(R);
+    std::iota(lo.begin(), lo.end(), 0);
+    std::iota(hi.begin(), hi.end(), 0);
+    std::vector<int64_t> rodA(d.nbind), rodB(d.nbind);
+    for (int64_t k = 0; k < d.nbind; ++k) {
+        const int64_t a = d.bind_a[k], b = d.bind_b[k];
+        if (a < 0 || a >= P || b < 0 || b >= P)
+            return fail(RS_E_INVALID, "binding %lld endpoint out of range", (long long)k);
+        rodA[k] = rod_of(d, a);
+        rodB[k] = rod_of(d, b);
+    }
+    // reach[r] = furthest rod that must share a segment with r
+    std::vector<int> reach(R);
+    std::iota(reach.begin(), reach.end(), 0);
+    for (int64_t k = 0; k < d.nbind; ++k) {
+        const int a = int(std::min(rodA[k], rodB[k])), b = int(std::max(rodA[k], rodB[k]));
+        reach[a] = std::max(reach[a], b);
+    }
+    std::vector<Segment> segs;
+    for (int r = 0; r < R;) {
+        int end = reach[r];
+        for (int x = r; x <= end; ++x) end = std::max(end, reach[x]);
+        segs.push_back({r, end, d.rod_offsets[r], d.rod_offsets[end + 1]});
+        r = end + 1;
+    }
+
+    // -- choose tiers --------------------------------------------------------
+    const int cta_cap = kVariants[kNumVariants - 1].CAP;
+    std::vector<int> seg_tier(segs.size());
+    int64_t max_cta_seg = 0;
+    for (size_t i = 0; i < segs.size(); ++i) {
+        const int64_t np = segs[i].p1 - segs[i].p0;
+        int tier = np <= cta_cap ? TIER_CTA : (np <= int64_t(kMaxCluster) * cta_cap ? TIER_CLUSTER : TIER_GRID);
+        if (d.force_tier >= 0) tier = d.force_tier;
+        if (tier == TIER_CTA && np > cta_cap)
+            return fail(RS_E_INVALID, "segment of %lld points does not fit one CTA", (long long)np);
+        if (tier == TIER_GRID) {
+            if (segs[i].r0 != segs[i].r1)
+                return fail(RS_E_UNSUPPORTED, "coupled rods larger than a %d-CTA cluster", kMaxCluster);
+        }
+        seg_tier[i] = tier;
+        if (tier == TIER_CTA) max_cta_seg = std::max(max_cta_seg, np);
+    }
+
+    for (Group& g : h->groups) {
+        if (g.d_flags) cudaFree(g.d_flags);
+        if (g.d_halo) cudaFree(g.d_halo);
+    }
+    h->h_tasks.clear();
+    h->h_binds.clear();
+    h->h_drvs.clear();
+    h->groups.clear();
+
+    // point -> (task, slot) for bindings and drivers
+    std::vector<int32_t> task_of(P, -1);
+
+    auto new_task = [&](int64_t p0, int64_t np) {
+        CtaTask t{};
+        t.p0 = int32_t(p0);
+        t.np = int32_t(np);
+        t.e_uni = -1;
+        for (int64_t p = p0; p < p0 + np; ++p) task_of[p] = int32_t(h->h_tasks.size());
+        h->h_tasks.push_back(t);
+    };
+
+    // CTA tier: pack consecutive CTA-tier segments into CTAs
+    if (max_cta_seg > 0) {
+        int v = 0;
+        while (kVariants[v].CAP < max_cta_seg) ++v;
+        if (d.force_variant >= 0) {
+            if (d.force_variant >= kNumVariants || kVariants[d.force_variant].CAP < max_cta_seg)
+                return fail(RS_E_INVALID, "force_variant %d cannot hold %lld points", d.force_variant,
+                            (long long)max_cta_seg);
+            v = d.force_variant;
+        }
+        Group g;
+        g.tier = TIER_CTA;
+        g.variant = v;
+        g.task_begin = int(h->h_tasks.size());
+        const int cap = kVariants[v].CAP;
+        int64_t cur0 = -1, cur1 = -1;
+        for (size_t i = 0; i < segs.size(); ++i) {
+            if (seg_tier[i] != TIER_CTA) {
+                if (cur0 >= 0) new_task(cur0, cur1 - cur0);
+                cur0 = -1;
+                continue;
+            }
+            const int64_t np = segs[i].p1 - segs[i].p0;
+            if (cur0 >= 0 && (cur1 - cur0) + np <= cap) {
+                cur1 = segs[i].p1;
+            } else {
+                if (cur0 >= 0) new_task(cur0, cur1 - cur0);
+                cur0 = segs[i].p0;
+                cur1 = segs[i].p1;
+            }
+        }
+        if (cur0 >= 0) new_task(cur0, cur1 - cur0);
+        g.ncta = int(h->h_tasks.size()) - g.task_begin;
+        h->groups.push_back(g);
+    }
+    // cluster / grid tiers: one launch per segment
+    for (size_t i = 0; i < segs.size(); ++i) {
+        if (seg_tier[i] == TIER_CTA) continue;
+        const int64_t np = segs[i].p1 - segs[i].p0;
+        Group g;
+        g.tier = seg_tier[i];
+        g.variant = kClusterVariant;
+        if (d.force_variant == 2 || d.force_variant == 4) g.variant = d.force_variant;
+        const int cap = kVariants[g.variant].CAP;
+        int c = int((np + cap - 1) / cap);
+        if (d.force_ctas > 0) c = std::max(c, int(d.force_ctas));
+        c = int(std::min<int64_t>(c, np));
+        if (g.tier == TIER_CLUSTER && c > kMaxCluster)
+            return fail(RS_E_UNSUPPORTED, "rod needs %d CTAs, more than a %d-CTA cluster", c, kMaxCluster);
+        if (c < 1) c = 1;
+        g.task_begin = int(h->h_tasks.size());
+        // balanced split, sizes differ by at most one (partition.py:39-51)
+        const int64_t base = np / c, rem = np % c;
+        int64_t p = segs[i].p0;
+        for (int k = 0; k < c; ++k) {
+            const int64_t sz = base + (k < rem ? 1 : 0);
+            new_task(p, sz);
+            p += sz;
+        }
+        g.ncta = c;
+        g.cluster = g.tier == TIER_CLUSTER ? c : 1;
+        h->groups.push_back(g);
+    }
+
+    // -- bindings ------------------------------------------------------------
+    // group the binding list by segment, keeping the reference order
+    std::vector<int> seg_of_rod(R);
+    for (size_t i = 0; i < segs.size(); ++i)
+        for (int r = segs[i].r0; r <= segs[i].r1; ++r) seg_of_rod[r] = int(i);
+    std::vector<std::vector<int64_t>> seg_binds(segs.size());
+    for (int64_t k = 0; k < d.nbind; ++k) seg_binds[seg_of_rod[rodA[k]]].push_back(k);
+    std::vector<std::vector<BindEntry>> per_task(h->h_tasks.size());
+    std::vector<int> task_seq(h->h_tasks.size(), 0);
+    std::vector<uint8_t> used(P, 0);
+    for (size_t i = 0; i < segs.size(); ++i) {
+        if (seg_binds[i].empty()) continue;
+        bool matching = true;
+        for (int64_t k : seg_binds[i]) {
+            const int64_t a = d.bind_a[k], b = d.bind_b[k];
+            if (used[a] || used[b] || a == b) matching = false;
+            used[a] = used[b] = 1;
+        }
+        for (int64_t k : seg_binds[i]) used[d.bind_a[k]] = used[d.bind_b[k]] = 0;
+        const int ta = task_of[segs[i].p0];
+        const Group* gp = nullptr;
+        for (const Group& g : h->groups)
+            if (ta >= g.task_begin && ta < g.task_begin + g.ncta) gp = &g;
+        for (int64_t k : seg_binds[i]) {
+            const int64_t a = d.bind_a[k], b = d.bind_b[k];
+            const int tka = task_of[a], tkb = task_of[b];
+            BindEntry be{};
+            be.a_rank = gp->tier == TIER_CLUSTER ? tka - gp->task_begin : 0;
+            be.b_rank = gp->tier == TIER_CLUSTER ? tkb - gp->task_begin : 0;
+            be.a_slot = int32_t(a - h->h_tasks[tka].p0);
+            be.b_slot = int32_t(b - h->h_tasks[tkb].p0);
+            be.mode = int32_t(d.bind_mode[k]);
+            if (gp->tier == TIER_CTA && tka != tkb)
+                return fail(RS_E_INVALID, "internal: binding split across CTAs");
+            // parallel: the CTA owning `a` applies it; sequential: rank 0
+            const int owner = matching ? tka : (gp->tier == TIER_CLUSTER ? gp->task_begin : tka);
+            per_task[owner].push_back(be);
+            if (!matching) task_seq[owner] = 1;
+        }
+    }
+    for (size_t t = 0; t < h->h_tasks.size(); ++t) {
+        h->h_tasks[t].bind_begin = int32_t(h->h_binds.size());
+        h->h_tasks[t].bind_count = int32_t(per_task[t].size());
+        h->h_tasks[t].bind_seq = task_seq[t];
+        h->h_binds.insert(h->h_binds.end(), per_task[t].begin(), per_task[t].end());
+    }
+
+    // -- drivers (rod order; the last rod driving a point wins) -------------
+    std::vector<std::vector<DrvEntry>> per_drv(h->h_tasks.size());
+    auto add_drv = [&](int64_t p, int kind, int64_t r) -> int {
+        if (p < 0) return RS_OK;
+        if (p >= P) return fail(RS_E_INVALID, "driver index out of range");
+        int64_t slot_p = p;
+        if (kind == 1) {   // frame e lives in the slot of its lower point
+            if (p >= d.E) return fail(RS_E_INVALID, "driven frame out of range");
+            slot_p = d.elem_point[p];
+        }
+        const int t = task_of[slot_p];
+        const int slot = int(slot_p - h->h_tasks[t].p0);
+        auto& v = per_drv[t];
+        const uint32_t bit = kind == 0 ? SF_DRV_PT : SF_DRV_FR;
+        const int shift = kind == 0 ? SF_DRV_PT_SHIFT : SF_DRV_FR_SHIFT;
+        if (pflags[slot_p] & bit) {   // already driven: later rod overrides
+            const int idx = int((pflags[slot_p] >> shift) & 0xffu);
+            v[idx].rod = int32_t(r);
+            return RS_OK;
+        }
+        if (int(v.size()) >= MAX_DRV_PER_CTA) return fail(RS_E_UNSUPPORTED, "too many drivers in one CTA");
+        DrvEntry e{};
+        e.slot = slot;
+        e.kind = kind;
+        e.rod = int32_t(r);
+        pflags[slot_p] |= bit | (uint32_t(v.size()) << shift);
+        v.push_back(e);
+        return RS_OK;
+    };
+    for (int64_t r = 0; r < R; ++r) {
+        int rc = add_drv(d.drv_pt[r], 0, r);
+        if (rc) return rc;
+        rc = add_drv(d.drv_fr[r], 1, r);
+        if (rc) return rc;
+    }
+    for (size_t t = 0; t < h->h_tasks.size(); ++t) {
+        h->h_tasks[t].drv_begin = int32_t(h->h_drvs.size());
+        h->h_tasks[t].drv_count = int32_t(per_drv[t].size());
+        h->h_drvs.insert(h->h_drvs.end(), per_drv[t].begin(), per_drv[t].end());
+    }
+
+    // -- per-launch uniformity, sizes and occupancy checks -------------------
+    for (Group& g : h->groups) {
+        const Variant var = kVariants[g.variant];
+        bool uni = true;
+        int max_np = 0, bcap = 0, dcap = 0;
+        for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
+            CtaTask& tk = h->h_tasks[t];
+            max_np = std::max(max_np, tk.np);
+            bcap = std::max(bcap, tk.bind_seq ? 0 : tk.bind_count);
+            dcap = std::max(dcap, tk.drv_count);
+            int64_t e0 = -1;
+            for (int64_t p = tk.p0; p < tk.p0 + tk.np; ++p) {
+                if (pt_elem[p] < 0) continue;
+                if (e0 < 0) {
+                    e0 = pt_elem[p];
+                } else if (uni && !elem_consts_equal(d, e0, pt_elem[p])) {
+                    uni = false;
+                }
+            }
+            tk.e_uni = int32_t(std::max<int64_t>(e0, 0));
+        }
+        g.uni = uni;
+        g.bind_cap = bcap;
+        g.drv_cap = std::max(dcap, 1);
+        const int maxT = var.CAP / var.S;
+        g.threads = std::min(maxT, ((max_np + var.S - 1) / var.S + 31) / 32 * 32);
+        g.threads = std::max(g.threads, 32);
+        size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap).total
+                                        : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap).total;
+        if (smem > kMaxSmem && g.bind_cap > 0) {
+            // no room to stage binding constants: apply bindings in order
+            for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
+                CtaTask& tk = h->h_tasks[t];
+                if (tk.bind_count == 0) continue;
+                if (g.tier == TIER_CLUSTER && t != g.task_begin)
+                    return fail(RS_E_UNSUPPORTED, "bindings too many for shared memory in cluster");
+                tk.bind_seq = 1;
+            }
+            g.bind_cap = 0;
+            smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, 0, g.drv_cap).total
+                                     : SmemLayout<double>(var.CAP, 0, g.drv_cap).total;
+        }
+        if (smem > kMaxSmem) return fail(RS_E_UNSUPPORTED, "shared memory plan %zu B too large", smem);
+        g.smem = smem;
+        int occ = 0;
+        int rc = occupancy_query(h, g.variant, g.tier, g.uni, g.threads, g.smem, g.cluster, &occ);
+        if (rc) return rc;
+        if (g.tier == TIER_CLUSTER && occ < 1)
+            return fail(RS_E_UNSUPPORTED, "a %d-CTA cluster of %zu B smem cannot be resident", g.cluster, g.smem);
+        if (g.tier == TIER_GRID && int64_t(occ) * h->num_sms < g.ncta)
+            return fail(RS_E_UNSUPPORTED, "grid tier needs %d co-resident CTAs, device holds %d", g.ncta,
+                        occ * h->num_sms);
+        if (g.tier == TIER_CTA && occ < 1)
+            return fail(RS_E_UNSUPPORTED, "CTA plan cannot be resident (%zu B smem, %d threads)", g.smem,
+                        g.threads);
+        if (g.tier == TIER_GRID) {
+            CK(cudaMalloc(&g.d_flags, sizeof(int32_t) * g.ncta));
+            CK(cudaMalloc(&g.d_halo, h->rsz * 2 * HALO_WORDS * size_t(g.ncta)));
+            CK(cudaMemset(g.d_halo, 0, h->rsz * 2 * HALO_WORDS * size_t(g.ncta)));
+        }
+    }
+
+    // sorted p0 index for grab placement
+    h->task_by_p0.resize(h->h_tasks.size());
+    std::iota(h->task_by_p0.begin(), h->task_by_p0.end(), 0);
+    std::sort(h->task_by_p0.begin(), h->task_by_p0.end(),
+              [&](int a, int b) { return h->h_tasks[a].p0 < h->h_tasks[b].p0; });
+    h->task_p0_sorted.resize(h->h_tasks.size());
+    for (size_t i = 0; i < h->task_by_p0.size(); ++i) h->task_p0_sorted[i] = h->h_tasks[h->task_by_p0[i]].p0;
+    h->task_group.assign(h->h_tasks.size(), 0);
+    for (size_t gi = 0; gi < h->groups.size(); ++gi)
+        for (int t = h->groups[gi].task_begin; t < h->groups[gi].task_begin + h->groups[gi].ncta; ++t)
+            h->task_group[t] = int(gi);
+    h->planned = true;
+    return RS_OK;
+}
+
+int find_task(rs_handle h, int64_t p) {
+    auto it = std::upper_bound(h->task_p0_sorted.begin(), h->task_p0_sorted.end(), p);
+    const int i = int(it - h->task_p0_sorted.begin()) - 1;
+    if (i < 0) return -1;
+    const int t = h->task_by_p0[i];
+    const CtaTask& tk = h->h_tasks[t];
+    return (p >= tk.p0 && p < tk.p0 + tk.np) ? t : -1;
+}
+
+// Rebuild the per-CTA grab tables from the World's grab slots.
+int build_grabs(rs_handle h) {
+    const rs_world_desc& d = h->d;
+    std::vector<std::vector<GrabEntry>> per(h->h_tasks.size());
+    for (int64_t k = 0; k < d.ngrab; ++k) {
+        if (!d.g_act[k]) continue;
+        const int64_t p = d.g_pt[k];
+        if (p < 0 || p >= d.P) return fail(RS_E_INVALID, "active grab %lld has no point", (long long)k);
+        const int t = find_task(h, p);
+        if (t < 0) return fail(RS_E_INVALID, "internal: grab point unplaced");
+        GrabEntry g{};
+        g.slot = int32_t(p - h->h_tasks[t].p0);
+        g.world_slot = int32_t(k);
+        for (int c = 0; c < 3; ++c) g.tgt[c] = d.g_tgt[3 * k + c];
+        if (per[t].size() >= size_t(GRAB_SM)) return fail(RS_E_UNSUPPORTED, "too many grabs in one CTA");
+        per[t].push_back(g);
+    }
+    h->h_grabs.clear();
+    for (size_t t = 0; t < h->h_tasks.size(); ++t) {
+        h->h_tasks[t].grab_begin = int32_t(h->h_grabs.size());
+        h->h_tasks[t].grab_count = int32_t(per[t].size());
+        h->h_grabs.insert(h->h_grabs.end(), per[t].begin(), per[t].end());
+    }
+    int rc = put_vec(h, h->grabs, h->h_grabs);
+    if (rc) return rc;
+    return put_vec(h, h->tasks, h->h_tasks);
+}
+
+int upload_static(rs_handle h) {
+    const rs_world_desc& d = h->d;
+    std::vector<uint32_t> pflags;
+    std::vector<int32_t> pt_elem;
+    int rc = plan(h, pflags, pt_elem);
+    if (rc) return rc;
+    const size_t P = size_t(d.P), E = size_t(d.E), R = size_t(d.R);
+    if ((rc = put_real(h, h->rest, d.rest, E))) return rc;
+    if ((rc = put_real(h, h->ustar, d.ustar, 3 * E))) return rc;
+    if ((rc = put_real(h, h->inert, d.inert, 3 * E))) return rc;
+    if ((rc = put_real(h, h->ks, d.ks, E))) return rc;
+    if ((rc = put_real(h, h->kp, d.kp, E))) return rc;
+    if ((rc = put_real(h, h->gt, d.gt, E))) return rc;
+    if ((rc = put_real(h, h->gr, d.gr, E))) return rc;
+    if ((rc = put_real(h, h->kb, d.kb, 3 * E))) return rc;
+    if ((rc = put_real(h, h->mass, d.mass, P))) return rc;
+    if ((rc = put_real(h, h->invm, d.invm, P))) return rc;
+    h->has_fext = 0;
+    for (size_t i = 0; i < 3 * P; ++i)
+        if (d.fext[i] != 0.0 || std::signbit(d.fext[i])) {
+            h->has_fext = 1;
+            break;
+        }
+    if (h->has_fext) {
+        if ((rc = put_real(h, h->fext, d.fext, 3 * P))) return rc;
+    } else if ((rc = dev_alloc(h->fext, h->rsz))) {
+        return rc;
+    }
+    (void)R;
+    if ((rc = put_vec(h, h->pflags, pflags))) return rc;
+    if ((rc = put_vec(h, h->pt_elem, pt_elem))) return rc;
+    if ((rc = put_vec(h, h->binds, h->h_binds))) return rc;
+    if ((rc = put_vec(h, h->drvs, h->h_drvs))) return rc;
+    return build_grabs(h);
+}
+
+int upload_control(rs_handle h) {
+    const rs_world_desc& d = h->d;
+    int rc = put_real(h, h->drv_v, d.drv_v, 3 * size_t(d.R));
+    if (rc) return rc;
+    if ((rc = put_real(h, h->drv_rot, d.drv_rot, size_t(d.R)))) return rc;
+    if (!h->planned) return RS_OK;
+    return build_grabs(h);
+}
+
+int upload_state(rs_handle h) {
+    const rs_world_desc& d = h->d;
+    int rc = put_real(h, h->pos, d.pos, 3 * size_t(d.P));
+    if (rc) return rc;
+    if ((rc = put_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
+    if ((rc = put_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
+    return put_real(h, h->w, d.w, 3 * size_t(d.E));
+}
+
+// Apply staged commands at the step boundary (ph_boundary, _core.pyx:477-506).
+void drain_ring(rs_handle h) {
+    std::lock_guard<std::mutex> lk(h->ring_mu);
+    rs_world_desc& d = h->d;
+    while (h->head < h->tail) {
+        const int slot = int(h->head % kRingCap);
+        const double* r = h->ring[slot];
+        const int op = int(r[0]);
+        const int64_t i0 = int64_t(r[1]), i1 = int64_t(r[2]);
+        if (op == 0 && i0 >= 0 && i0 < d.R) {
+            for (int k = 0; k < 3; ++k) d.drv_v[3 * i0 + k] = r[3 + k];
+        } else if (op == 1 && i0 >= 0 && i0 < d.R) {
+            d.drv_rot[i0] = r[3];
+        } else if (op == 2 && i0 >= 0 && i0 < d.ngrab) {
+            d.g_pt[i0] = i1;
+            for (int k = 0; k < 3; ++k) d.g_tgt[3 * i0 + k] = r[3 + k];
+            d.g_act[i0] = 1;
+        } else if (op == 3 && i0 >= 0 && i0 < d.ngrab) {
+            d.g_act[i0] = 0;
+            d.g_pt[i0] = -1;
+        }
+        h->ring_apply[slot] = h->step;
+        h->head += 1;
+        h->control_dirty = true;
+    }
+}
+
+template <typename Real>
+StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) {
+    StepArgs<Real> a{};
+    a.pos = static_cast<Real*>(h->pos.p);
+    a.vel = static_cast<Real*>(h->vel.p);
+    a.q = static_cast<Real*>(h->q.p);
+    a.w = static_cast<Real*>(h->w.p);
+    a.rest = static_cast<const Real*>(h->rest.p);
+    a.ustar = static_cast<const Real*>(h->ustar.p);
+    a.inert = static_cast<const Real*>(h->inert.p);
+    a.ks = static_cast<const Real*>(h->ks.p);
+    a.kp = static_cast<const Real*>(h->kp.p);
+    a.gt = static_cast<const Real*>(h->gt.p);
+    a.gr = static_cast<const Real*>(h->gr.p);
+    a.kb = static_cast<const Real*>(h->kb.p);
+    a.mass = static_cast<const Real*>(h->mass.p);
+    a.invm = static_cast<const Real*>(h->invm.p);
+    a.fext = static_cast<const Real*>(h->fext.p);
+    a.drv_v = static_cast<const Real*>(h->drv_v.p);
+    a.drv_rot = static_cast<const Real*>(h->drv_rot.p);
+    a.pflags = static_cast<const uint32_t*>(h->pflags.p);
+    a.pt_elem = static_cast<const int32_t*>(h->pt_elem.p);
+    a.tasks = static_cast<const CtaTask*>(h->tasks.p) + g.task_begin;
+    a.binds = static_cast<const BindEntry*>(h->binds.p);
+    a.grabs = static_cast<const GrabEntry*>(h->grabs.p);
+    a.drvs = static_cast<const DrvEntry*>(h->drvs.p);
+    a.flags = g.d_flags;
+    a.halo = static_cast<Real*>(g.d_halo);
+    a.err_step = h->d_err;
+    a.step0 = step0;
+    a.steps = steps;
+    a.iters = int32_t(h->d.iters);
+    a.bind_cap = g.bind_cap;
+    a.drv_cap = g.drv_cap;
+    a.has_fext = h->has_fext;
+    a.ncta = g.ncta;
+    a.debug = h->debug;
+    a.dt = Real(h->d.dt);
+    a.beta = Real(h->d.beta);
+    a.gx = Real(h->d.gx);
+    a.gy = Real(h->d.gy);
+    a.gz = Real(h->d.gz);
+    return a;
+}
+
+int launch_group(rs_handle h, const Group& g, int64_t step0, int steps) {
+    if (g.tier == TIER_GRID) CK(cudaMemsetAsync(g.d_flags, 0, sizeof(int32_t) * g.ncta, h->st));
+    cudaError_t e;
+    if (h->prec == RS_F64_MIRROR) {
+        auto a = make_args<double>(h, g, step0, steps);
+        e = mirror::launch_step<double>(g.variant, g.tier, g.uni, a, g.ncta, g.threads, g.smem, g.cluster, h->st);
+    } else if (h->prec == RS_F32) {
+        auto a = make_args<float>(h, g, step0, steps);
+        e = fast::launch_step<float>(g.variant, g.tier, g.uni, a, g.ncta, g.threads, g.smem, g.cluster, h->st);
+    } else {
+        auto a = make_args<double>(h, g, step0, steps);
+        e = fast::launch_step<double>(g.variant, g.tier, g.uni, a, g.ncta, g.threads, g.smem, g.cluster, h->st);
+    }
+    if (e != cudaSuccess)
+        return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
+                    g.tier, g.variant, g.ncta, g.threads, g.smem, cudaGetErrorString(e));
+    h->launches += 1;
+    return RS_OK;
+}
+
+void register_host(rs_handle h, void* p, size_t bytes) {
+    if (!p || bytes < (size_t(1) << 20)) return;
+    if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess)
+        h->registered.push_back(p);
+    else
+        cudaGetLastError();
+}
+
+}  // namespace
+
+// ---- C ABI --------------------------------------------------------------------
+
+extern "C" {
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+int rs_create(const rs_world_desc* desc, rs_handle* out) {
+    if (!desc || !out) return fail(RS_E_INVALID, "null argument");
+    *out = nullptr;
+    if (desc->abi_version != RS_ABI_VERSION) return fail(RS_E_INVALID, "ABI version mismatch");
+    if (desc->P < 2 || desc->R < 1 || desc->E != desc->P - desc->R)
+        return fail(RS_E_INVALID, "inconsistent world sizes");
+    if (desc->dt <= 0.0 || desc->iters < 1) return fail(RS_E_INVALID, "dt must be positive and iters >= 1");
+    if (desc->precision < 0 || desc->precision > 2) return fail(RS_E_INVALID, "unknown precision");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (desc->device < 0 || desc->device >= ndev) return fail(RS_E_INVALID, "no CUDA device %d", desc->device);
+    CK(cudaSetDevice(desc->device));
+    auto h = new rs_handle_s();
+    h->d = *desc;
+    h->prec = desc->precision;
+    h->rsz = h->prec == RS_F32 ? sizeof(float) : sizeof(double);
+    h->step = desc->step_index;
+    if (const char* dbg = getenv("RSB_DEBUG")) h->debug = atoi(dbg);
+    for (int i = 0; i < kRingCap; ++i) h->ring_apply[i] = -1;
+    int rc = RS_OK;
+    auto bail = [&](int code) {
+        rs_destroy(h);
+        return code;
+    };
+    if (cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, desc->device) != cudaSuccess)
+        return bail(fail(RS_E_CUDA, "device query failed"));
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess ||
+        cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&h->h_err, sizeof(unsigned long long)) != cudaSuccess)
+        return bail(fail(RS_E_CUDA, "CUDA resource creation failed"));
+    *h->h_err = 0;
+    if (cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess)
+        return bail(fail(RS_E_CUDA, "memset failed"));
+    if (h->rsz == sizeof(double)) {
+        register_host(h, h->d.pos, 3 * sizeof(double) * size_t(h->d.P));
+        register_host(h, h->d.vel, 3 * sizeof(double) * size_t(h->d.P));
+        register_host(h, h->d.q, 4 * sizeof(double) * size_t(h->d.E));
+        register_host(h, h->d.w, 3 * sizeof(double) * size_t(h->d.E));
+    }
+    if ((rc = upload_control(h))) return bail(rc);
+    if ((rc = upload_static(h))) return bail(rc);
+    if ((rc = upload_state(h))) return bail(rc);
+    if (cudaStreamSynchronize(h->st) != cudaSuccess) return bail(fail(RS_E_CUDA, "sync failed"));
+    h->snap_seq = 2;
+    h->snap_step = h->step;
+    *out = h;
+    return RS_OK;
+}
+
+int rs_upload(rs_handle h, uint32_t mask) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    CK(cudaSetDevice(h->d.device));
+    int rc = RS_OK;
+    if (mask & RS_CONTROL) {
+        if ((rc = upload_control(h))) return rc;
+        h->control_dirty = false;
+    }
+    if (mask & RS_STATIC) {
+        CK(cudaStreamSynchronize(h->st));
+        if ((rc = upload_static(h))) return rc;
+    }
+    if (mask & RS_STATE)
+        if ((rc = upload_state(h))) return rc;
+    return RS_OK;
+}
+
+int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
+    CK(cudaSetDevice(h->d.device));
+    drain_ring(h);
+    if (h->control_dirty) {
+        int rc = upload_control(h);
+        if (rc) return rc;
+        h->control_dirty = false;
+    }
+    if (h->timing) CK(cudaEventRecord(h->ev0, h->st));
+    int64_t done = 0;
+    while (done < steps) {
+        const int k = int(std::min<int64_t>(steps - done, kMaxStepsPerLaunch));
+        for (const Group& g : h->groups) {
+            int rc = launch_group(h, g, h->step + done, k);
+            if (rc) return rc;
+        }
+        done += k;
+    }
+    if (h->timing) CK(cudaEventRecord(h->ev1, h->st));
+    h->timed = h->timing;
+    CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+    h->step += steps;
+    h->snap_seq += 2 * steps;
+    h->snap_step = h->step;
+    if (contacts) *contacts = 0;
+    if (barrier_ns) *barrier_ns = 0;
+    return RS_OK;
+}
+
+int rs_synchronize(rs_handle h) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    CK(cudaSetDevice(h->d.device));
+    CK(cudaStreamSynchronize(h->st));
+    if (*h->h_err) h->err_step = std::max<int64_t>(h->err_step, int64_t(*h->h_err) - 1);
+    if (h->timed) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        h->last_ms = ms;
+        h->timed = false;
+    }
+    return RS_OK;
+}
+
+int rs_download(rs_handle h, uint32_t mask) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    CK(cudaSetDevice(h->d.device));
+    const rs_world_desc& d = h->d;
+    int rc = RS_OK;
+    if (mask & RS_STATE) {
+        if ((rc = get_real(h, h->pos, d.pos, 3 * size_t(d.P)))) return rc;
+        if ((rc = get_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
+        if ((rc = get_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
+        if ((rc = get_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+    }
+    return rs_synchronize(h);
+}
+
+int64_t rs_error_step(rs_handle h) {
+    if (!h) return -1;
+    rs_synchronize(h);
+    return h->err_step;
+}
+
+int64_t rs_step_counter(rs_handle h) { return h ? h->step : -1; }
+
+int rs_update_params(rs_handle h, double dt, int64_t iters) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    if (dt <= 0.0 || iters < 1) return fail(RS_E_INVALID, "dt must be positive and iters >= 1");
+    h->d.dt = dt;
+    h->d.iters = iters;
+    return RS_OK;
+}
+
+int rs_stage_commands(rs_handle h, const double* ops, int64_t n, int64_t* slots) {
+    if (!h || (n > 0 && !ops)) return fail(RS_E_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(h->ring_mu);
+    for (int64_t i = 0; i < n; ++i) {
+        if (h->tail - h->head >= kRingCap)
+            return fail(RS_E_RING_FULL, "command ring full and not draining");
+        const int slot = int(h->tail % kRingCap);
+        h->ring_apply[slot] = -1;
+        std::memcpy(h->ring[slot], ops + 6 * i, 6 * sizeof(double));
+        if (slots) slots[i] = h->tail;
+        h->tail += 1;
+    }
+    return RS_OK;
+}
+
+int64_t rs_applied_step_for(rs_handle h, int64_t global_slot) {
+    if (!h) return -1;
+    std::lock_guard<std::mutex> lk(h->ring_mu);
+    return h->ring_apply[global_slot % kRingCap];
+}
+
+int rs_read_snapshot(rs_handle h, double* pos, double* q, int64_t* seq, int64_t* step) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    // the host arrays hold the state of the last completed download
+    if (pos) std::memcpy(pos, h->d.pos, sizeof(double) * 3 * size_t(h->d.P));
+    if (q) std::memcpy(q, h->d.q, sizeof(double) * 4 * size_t(h->d.E));
+    if (seq) *seq = h->snap_seq;
+    if (step) *step = h->snap_step;
+    return RS_OK;
+}
+
+void rs_destroy(rs_handle h) {
+    if (!h) return;
+    cudaSetDevice(h->d.device);
+    if (h->st) cudaStreamSynchronize(h->st);
+    for (DevBuf* b : {&h->pos, &h->vel, &h->q, &h->w, &h->rest, &h->ustar, &h->inert, &h->ks, &h->kp, &h->gt,
+                      &h->gr, &h->kb, &h->mass, &h->invm, &h->fext, &h->drv_v, &h->drv_rot, &h->pflags,
+                      &h->pt_elem, &h->tasks, &h->binds, &h->drvs, &h->grabs})
+        if (b->p) cudaFree(b->p);
+    for (Group& g : h->groups) {
+        if (g.d_flags) cudaFree(g.d_flags);
+        if (g.d_halo) cudaFree(g.d_halo);
+    }
+    for (void* p : h->registered) cudaHostUnregister(p);
+    if (h->d_err) cudaFree(h->d_err);
+    if (h->h_err) cudaFreeHost(h->h_err);
+    if (h->stage) cudaFreeHost(h->stage);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->st) cudaStreamDestroy(h->st);
+    delete h;
+}
+
+int rs_enable_timing(rs_handle h, int on) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    h->timing = on != 0;
+    return RS_OK;
+}
+
+double rs_last_kernel_ms(rs_handle h) {
+    if (!h) return -1.0;
+    rs_synchronize(h);
+    return h->last_ms;
+}
+
+int64_t rs_launch_count(rs_handle h) { return h ? h->launches : -1; }
+
+int rs_plan_json(rs_handle h, char* buf, int64_t len) {
+    if (!h || !buf || len <= 0) return fail(RS_E_INVALID, "bad argument");
+    std::string s = "{\"precision\": " + std::to_string(h->prec) + ", \"groups\": [";
+    for (size_t i = 0; i < h->groups.size(); ++i) {
+        const Group& g = h->groups[i];
+        const Variant v = kVariants[g.variant];
+        int64_t pts = 0;
+        for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) pts += h->h_tasks[t].np;
+        char tmp[512];
+        snprintf(tmp, sizeof tmp,
+                 "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "
+                 "\"uniform\": %s, \"ctas\": %d, \"threads\": %d, \"cluster\": %d, \"smem\": %zu, "
+                 "\"points\": %lld, \"bind_cap\": %d}",
+                 i ? ", " : "", g.tier == TIER_CTA ? "cta" : (g.tier == TIER_CLUSTER ? "cluster" : "grid"),
+                 g.variant, v.S, v.CAP, g.uni ? "true" : "false", g.ncta, g.threads, g.cluster, g.smem,
+                 (long long)pts, g.bind_cap);
+        s += tmp;
+    }
+    s += "]}";
+    if (int64_t(s.size()) + 1 > len) return fail(RS_E_INVALID, "buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return RS_OK;
+}
+
+int rs_device_ptr(rs_handle h, int32_t which, void** out) {
+    if (!h || !out) return fail(RS_E_INVALID, "null argument");
+    const DevBuf* b[] = {&h->pos, &h->vel, &h->q, &h->w};
+    if (which < 0 || which > 3) return fail(RS_E_INVALID, "unknown array");
+    *out = b[which]->p;
+    return RS_OK;
+}
+
+}  // extern "C"
+
+namespace rsb {
+namespace mirror {
+cudaError_t div_selftest(const double*, const double*, int64_t, double*, double*);
+}
+}  // namespace rsb
+
+extern "C" int rs_selftest_div(const double* a, const double* b, int64_t n, double* q_ieee,
+                               double* q_fast) {
+    double *da = nullptr, *db = nullptr, *dq = nullptr, *df = nullptr;
+    const size_t bytes = sizeof(double) * size_t(n);
+    CK(cudaMalloc(&da, bytes));
+    CK(cudaMalloc(&db, bytes));
+    CK(cudaMalloc(&dq, bytes));
+    CK(cudaMalloc(&df, bytes));
+    CK(cudaMemcpy(da, a, bytes, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, b, bytes, cudaMemcpyHostToDevice));
+    CK(rsb::mirror::div_selftest(da, db, n, dq, df));
+    CK(cudaMemcpy(q_ieee, dq, bytes, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(q_fast, df, bytes, cudaMemcpyDeviceToHost));
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dq);
+    cudaFree(df);
+    return RS_OK;
+}

@@ -1,0 +1,364 @@
+"""Epoch engine: steps a World on the B200 through the C ABI.
+
+Drop-in for the reference Engine (rodsim/engine.py:144-367): same
+constructor, `run_epoch` metrics dict, command tickets, command log,
+snapshot buffer and error surfacing.  Both reference backends ("serial",
+"parallel") map to the one GPU path -- a persistent sm_100a kernel that
+advances K = `steps` time steps per launch.  There is no CPU fallback: if
+the CUDA library or device is missing, constructing an Engine raises.
+
+Per epoch (the reference's epoch, _core.pyx:1091-1139):
+  1. queued commands are applied at the epoch's first step boundary and
+     logged with that step (the serial path's semantics, engine.py:265-270);
+  2. host arrays -> HBM (state every epoch; constants when they changed);
+  3. one launch per tier runs all K steps on-chip;
+  4. HBM -> host arrays; a recorded non-finite / degenerate step raises
+     FloatingPointError like the reference (engine.py:328-333).
+"""
+
+import queue
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .partition import partition_world
+
+OP_DRIVER_VELOCITY = 0
+OP_DRIVER_ROTATION = 1
+OP_GRAB = 2
+OP_RELEASE = 3
+
+# worlds at most this large re-check their constant arrays every epoch
+# (cheap); larger ones re-upload them when World.static_version changes
+SMALL_WORLD_POINTS = 1 << 14
+
+_STATIC_ATTRS = ("rest_lengths", "intrinsic_strains", "masses", "inv_masses",
+                 "inertias", "external_forces", "stretch_k", "penalty_k",
+                 "gamma_t", "gamma_r", "extensible", "bend_k", "point_locked",
+                 "frame_locked", "junction_valid", "elem_point", "elem_parity",
+                 "driven_point", "driven_frame", "bind_a", "bind_b",
+                 "bind_mode")
+_BOUND_ATTRS = _STATIC_ATTRS + ("positions", "velocities", "frames",
+                                "angular_velocities", "driver_velocity",
+                                "driver_rotation", "grab_active",
+                                "grab_point", "grab_target")
+
+
+@dataclass
+class Command:
+    name: str
+    args: dict
+    id: int = -1
+
+
+class Ticket:
+    """Resolved with the step index at which the command took effect."""
+
+    def __init__(self, command):
+        self.command = command
+        self._event = threading.Event()
+        self.apply_step = None
+
+    def resolve(self, step):
+        self.apply_step = step
+        self._event.set()
+
+    def wait(self, timeout=None):
+        if not self._event.wait(timeout):
+            raise TimeoutError("command not applied in time")
+        return self.apply_step
+
+
+class Mailbox:
+    """Multi-producer queue of steering commands."""
+
+    def __init__(self):
+        self._queue = queue.Queue()
+        self._next_id = 0
+        self._lock = threading.Lock()
+
+    def post(self, name, **args):
+        with self._lock:
+            cmd = Command(name, args, self._next_id)
+            self._next_id += 1
+        ticket = Ticket(cmd)
+        self._queue.put((cmd, ticket))
+        return ticket
+
+    def drain(self):
+        out = []
+        while True:
+            try:
+                out.append(self._queue.get_nowait())
+            except queue.Empty:
+                return out
+
+
+@dataclass
+class Snapshot:
+    sequence: int
+    step_index: int
+    positions: np.ndarray
+    frames: np.ndarray = None
+
+
+class SnapshotBuffer:
+    """Single-writer seqlock (odd sequence while a publish is in flight)."""
+
+    def __init__(self, world):
+        self.positions = np.zeros_like(world.positions)
+        self.frames = np.zeros_like(world.frames)
+        self.seq = np.zeros(1, dtype=np.int64)
+        self.step = np.zeros(1, dtype=np.int64)
+
+    def publish(self, world):
+        self.seq[0] += 1
+        self.positions[:] = world.positions
+        self.frames[:] = world.frames
+        self.step[0] = world.step_index
+        self.seq[0] += 1
+
+    def read(self, max_retries=100000):
+        for _ in range(max_retries):
+            s1 = int(self.seq[0])
+            if s1 % 2:
+                continue
+            pos, frames = self.positions.copy(), self.frames.copy()
+            step = int(self.step[0])
+            if int(self.seq[0]) == s1:
+                return Snapshot(s1, step, pos, frames)
+        raise RuntimeError("snapshot read kept tearing")
+
+
+class HaloTracker:
+    """Barrier-generation counters per block (stale-halo detection API,
+    engine.py:126-141).  On the device the barriers are bar.sync /
+    barrier.cluster / release-acquire flags; this host object is kept for
+    callers and tests of the reference API."""
+
+    def __init__(self, num_blocks):
+        self.generation = np.zeros(num_blocks, dtype=np.int64)
+
+    def barrier(self):
+        self.generation += 1
+
+    def check(self, block, neighbor):
+        if self.generation[block] != self.generation[neighbor]:
+            raise RuntimeError(
+                f"stale halo read: block {block} at generation "
+                f"{self.generation[block]}, neighbor {neighbor} at "
+                f"{self.generation[neighbor]}")
+        return True
+
+
+class Engine:
+    """Steps a World on the GPU (reference backends map to the same path)."""
+
+    def __init__(self, world, backend="serial", block_cap=512,
+                 use_compiled=None, max_blocks=None, precision="f64",
+                 device=0, force_tier=-1, force_ctas=0, force_variant=-1):
+        if backend not in ("serial", "parallel"):
+            raise ValueError("backend must be 'serial' or 'parallel'")
+        if world.tree is not None:
+            raise NotImplementedError(
+                "mesh contacts are not in this build's hot-path scope "
+                "(SURVEY.md §8(f) next #1)")
+        if world.self_collision_enabled:
+            raise NotImplementedError(
+                "self-collision is not in this build's hot-path scope "
+                "(SURVEY.md §8(f) next #2)")
+        self.world = world
+        self.backend = backend
+        self.precision = precision
+        self.device = device
+        self.partition = partition_world(world, block_cap, max_blocks=max_blocks)
+        self.mailbox = Mailbox()
+        self.snapshot_buffer = SnapshotBuffer(world)
+        self.halo = HaloTracker(self.partition.block_count)
+        self.command_log = []
+        self.last_contacts = 0
+        self.compiled = True       # the CUDA core is the only backend
+        self._pending = []
+        self._force = (force_tier, force_ctas, force_variant)
+        self._lock = threading.Lock()
+        self._dev = None
+        self._bind()
+        self.snapshot_buffer.publish(world)
+
+    # -- device handle -----------------------------------------------------
+
+    def _bind(self):
+        if self._dev is not None:
+            self._dev.close()
+        ft, fc, fv = self._force
+        self._dev = _lib.DeviceWorld(self.world, self.precision, self.device,
+                                     force_tier=ft, force_ctas=fc,
+                                     force_variant=fv)
+        self._bound = {a: getattr(self.world, a) for a in _BOUND_ATTRS}
+        self._static_version = self.world.static_version
+        self._small = self.world.num_points <= SMALL_WORLD_POINTS
+        self._static_copy = ({a: np.array(getattr(self.world, a), copy=True)
+                              for a in _STATIC_ATTRS} if self._small else None)
+
+    def _push(self):
+        """Host -> device before an epoch."""
+        w = self.world
+        if any(getattr(w, a) is not arr for a, arr in self._bound.items()):
+            # an array attribute was replaced: re-bind (re-plans and uploads)
+            self._bind()
+            return
+        static_dirty = w.static_version != self._static_version
+        if self._small and not static_dirty:
+            static_dirty = any(not np.array_equal(getattr(w, a), c)
+                               for a, c in self._static_copy.items())
+        mask = _lib.RS_STATE | _lib.RS_CONTROL
+        if static_dirty:
+            mask |= _lib.RS_STATIC
+            self._static_version = w.static_version
+            if self._small:
+                self._static_copy = {a: np.array(getattr(w, a), copy=True)
+                                     for a in _STATIC_ATTRS}
+        self._dev.upload(mask)
+
+    # -- commands ----------------------------------------------------------
+
+    def post_command(self, name, **args):
+        return self.mailbox.post(name, **args)
+
+    def _encode(self, cmd):
+        """Command -> [op, i0, i1, f0, f1, f2] rows (engine.py:200-226)."""
+        w, a = self.world, cmd.args
+        if cmd.name == "insert_velocity":
+            rod = a.get("rod", 0)
+            vel = float(a["value"]) * np.asarray(a.get("axis", self._driver_axis(rod)))
+            return [[OP_DRIVER_VELOCITY, rod, 0, vel[0], vel[1], vel[2]]]
+        if cmd.name == "rotate_velocity":
+            return [[OP_DRIVER_ROTATION, a.get("rod", 0), 0, float(a["value"]), 0.0, 0.0]]
+        if cmd.name == "grab":
+            rod = a.get("rod", 0)
+            point = w.rod_infos[rod].point_offset + int(a["index"])
+            t = np.asarray(a["target"], dtype=float)
+            return [[OP_GRAB, self._grab_slot(point), point, t[0], t[1], t[2]]]
+        if cmd.name == "release":
+            point = w.rod_infos[a.get("rod", 0)].point_offset + int(a["index"])
+            return [[OP_RELEASE, s, 0, 0.0, 0.0, 0.0]
+                    for s in range(w.grab_active.shape[0]) if w.grab_point[s] == point]
+        raise ValueError(f"unknown command {cmd.name!r}")
+
+    def _grab_slot(self, point):
+        w = self.world
+        for slot in range(w.grab_active.shape[0]):
+            if w.grab_point[slot] == point:
+                return slot
+        for slot in range(w.grab_active.shape[0]):
+            if not w.grab_active[slot] and w.grab_point[slot] == -1:
+                w.grab_point[slot] = point
+                return slot
+        raise RuntimeError("no free grab slot")
+
+    def _driver_axis(self, rod):
+        v = self.world.driver_velocity[rod]
+        n = np.linalg.norm(v)
+        return v / n if n > 0.0 else np.array([0.0, 0.0, 1.0])
+
+    def _apply_command(self, cmd):
+        w, a = self.world, cmd.args
+        if cmd.name == "insert_velocity":
+            rod = a.get("rod", 0)
+            w.driver_velocity[rod] = float(a["value"]) * np.asarray(
+                a.get("axis", self._driver_axis(rod)))
+        elif cmd.name == "rotate_velocity":
+            w.driver_rotation[a.get("rod", 0)] = float(a["value"])
+        elif cmd.name == "grab":
+            w.grab(a.get("rod", 0), int(a["index"]),
+                   np.asarray(a["target"], dtype=float))
+        elif cmd.name == "release":
+            w.release(a.get("rod", 0), int(a["index"]))
+        else:
+            raise ValueError(f"unknown command {cmd.name!r}")
+
+    def _drain_at_boundary(self):
+        for cmd, ticket in self.mailbox.drain():
+            self._apply_command(cmd)
+            self.command_log.append((self.world.step_index, cmd))
+            ticket.resolve(self.world.step_index)
+
+    def stage_commands(self, ops):
+        """Stage encoded ops on the device handle's ring; they apply at the
+        next epoch's first step boundary (rs_stage_commands)."""
+        return self._dev.stage_commands(ops)
+
+    def _resolve_applied(self):
+        still = []
+        for cmd, ticket, slot in self._pending:
+            step = self._dev.applied_step_for(slot)
+            if step >= 0:
+                self.command_log.append((step, cmd))
+                ticket.resolve(step)
+            else:
+                still.append((cmd, ticket, slot))
+        self._pending = still
+
+    # -- stepping ----------------------------------------------------------
+
+    def run_epoch(self, steps):
+        """Execute `steps` time steps (one persistent launch); metrics dict."""
+        if steps < 1:
+            raise ValueError("steps must be >= 1")
+        with self._lock:
+            t0 = time.perf_counter_ns()
+            self._drain_at_boundary()
+            self._push()
+            contacts, barrier_ns = self._dev.run(steps)
+            self._dev.download(_lib.RS_STATE)
+            self.world.step_index += steps
+            self._resolve_applied()
+            self.last_contacts = contacts
+            self.snapshot_buffer.publish(self.world)
+            self._check_core_error()
+            wall = time.perf_counter_ns() - t0
+        return {"wall_ns": wall, "steps": steps,
+                "barrier_wait_ns": barrier_ns, "contacts": contacts}
+
+    def _check_core_error(self):
+        step = self._dev.error_step()
+        if step >= 0:
+            raise FloatingPointError(
+                f"non-finite force/torque or degenerate geometry at step {step}")
+
+    def set_params(self, dt=None, iterations=None):
+        if dt is not None:
+            if dt <= 0.0:
+                raise ValueError("dt must be positive")
+            self.world.dt = float(dt)
+        if iterations is not None:
+            if iterations < 1:
+                raise ValueError("iterations must be >= 1")
+            self.world.solver.iterations = int(iterations)
+        self._dev.update_params(self.world.dt, self.world.solver.iterations)
+
+    def read_snapshot(self):
+        return self.snapshot_buffer.read()
+
+    # -- introspection -----------------------------------------------------
+
+    @property
+    def device_world(self):
+        return self._dev
+
+    def plan(self):
+        return self._dev.plan()
+
+    def close(self):
+        if self._dev is not None:
+            self._dev.close()
+            self._dev = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

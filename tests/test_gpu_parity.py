@@ -1,0 +1,256 @@
+"""GPU parity: the sm_100a step against the CPU oracle (oracle/rod_oracle.c,
+itself pinned bit-for-bit to the reference core by test_oracle.py).
+
+fp64 mirror mode: bitwise equality of positions, velocities, frames and
+angular velocities after N steps (np.array_equal), for every tier (CTA,
+cluster, grid), epoch split K, drivers, bindings, grabs and commands.
+fp32 mode: max|dr| <= 1e-5 L and max|dq| <= 1e-4 after 1000 steps on the
+well-conditioned configs; the chaotic pair at 10 steps.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2509_04277_b200 import state as st
+from paper_2509_04277_b200 import workloads as wl
+from paper_2509_04277_b200.constraints import SolverConfig
+from paper_2509_04277_b200.engine import Engine
+from paper_2509_04277_b200.world import BIND_BIDIRECTIONAL, BIND_ONE_WAY, World
+
+from oracle.oracle import OracleStepper
+
+pytestmark = pytest.mark.gpu
+
+STATE = ("positions", "velocities", "frames", "angular_velocities")
+
+
+def _diff(a, b):
+    return {k: float(np.max(np.abs(getattr(a, k) - getattr(b, k)))) for k in STATE}
+
+
+def assert_bitwise(gpu_world, ref_world):
+    same = {k: np.array_equal(getattr(gpu_world, k), getattr(ref_world, k)) for k in STATE}
+    assert all(same.values()), f"not bitwise: {same} max|d| {_diff(gpu_world, ref_world)}"
+
+
+def run_gpu(world, steps, k, **kw):
+    with Engine(world, **kw) as eng:
+        done = 0
+        while done < steps:
+            n = min(k, steps - done)
+            eng.run_epoch(n)
+            done += n
+        return eng.plan()
+
+
+def parity(make, steps, k=None, **kw):
+    g, r = make(), make()
+    run_gpu(g, steps, k or steps, **kw)
+    OracleStepper(r).run(steps)
+    assert_bitwise(g, r)
+    assert g.step_index == r.step_index == steps
+    return g
+
+
+# -- BASELINE configs (fp64 mirror: bitwise) ----------------------------------
+
+def test_cfg1_cantilever_1000_steps_bitwise():
+    w = parity(wl.cantilever, 1000)
+    assert w.max_strain() < 1e-2
+
+
+@pytest.mark.parametrize("k", [1, 10, 100])
+def test_cfg1_bitwise_independent_of_epoch_size(k):
+    parity(wl.cantilever, 200, k)
+
+
+def test_cfg2_extensible_512_k10_bitwise():
+    parity(wl.extensible, 300, 10)
+
+
+def test_cfg3_pair_bitwise_300_steps():
+    g = parity(wl.pair, 300, 10)
+    assert g.max_strain() < 0.1
+
+
+@pytest.mark.parametrize("n", [16, 64, 256, 1024])
+def test_cfg4_sweep_cta_tier_bitwise(n):
+    parity(lambda: wl.sweep(n), 50, 25)
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 16384])
+def test_cfg4_sweep_cluster_tier_bitwise(n):
+    g, r = wl.sweep(n), wl.sweep(n)
+    plan = run_gpu(g, 20, 10)
+    assert plan["groups"][0]["tier"] == "cluster"
+    OracleStepper(r).run(20)
+    assert_bitwise(g, r)
+
+
+def test_cfg4_grid_tier_bitwise():
+    # 32768 elements exceed a 16-CTA cluster: cooperative grid tier
+    g, r = wl.sweep(32768), wl.sweep(32768)
+    plan = run_gpu(g, 6, 3)
+    assert plan["groups"][0]["tier"] == "grid"
+    OracleStepper(r).run(6)
+    assert_bitwise(g, r)
+
+
+def test_cfg5_hair_sample_bitwise():
+    parity(lambda: wl.hair(16), 200, 50)
+
+
+# -- forced tiers on small rods (exercise DSMEM / halo paths cheaply) ---------
+
+@pytest.mark.parametrize("ctas", [2, 3, 5, 8, 16])
+def test_forced_cluster_tier_bitwise(ctas):
+    parity(lambda: wl.cantilever(200, 0.4), 60, 20, force_tier=1, force_ctas=ctas)
+
+
+@pytest.mark.parametrize("ctas", [2, 3, 7])
+def test_forced_grid_tier_bitwise(ctas):
+    parity(lambda: wl.cantilever(200, 0.4), 60, 20, force_tier=2, force_ctas=ctas)
+
+
+def test_forced_cluster_pair_with_bindings_bitwise():
+    parity(lambda: wl.pair(100, 0.2), 100, 10, force_tier=1, force_ctas=4)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_cta_variants_bitwise(variant):
+    parity(lambda: wl.cantilever(100, 0.2), 100, 50, force_variant=variant)
+
+
+def test_many_rods_packed_per_cta_bitwise():
+    def make():
+        w = World(dt=1e-4, solver=SolverConfig(iterations=6))
+        rng = np.random.default_rng(3)
+        for r in range(40):
+            n = int(rng.integers(2, 70))
+            w.add_rod(st.init_rod(n, 0.002 * n, axis=rng.normal(size=3),
+                                  origin=rng.normal(size=3) * 0.1),
+                      st.RodParams(**wl.MATERIAL))
+        w.finalize()
+        for r in range(0, 40, 3):
+            w.clamp_point(r, 0)
+        return w
+    parity(make, 100, 33)
+
+
+# -- controls -----------------------------------------------------------------
+
+def _scene(bindings=None, n=40, rods=2):
+    w = World(dt=1e-4, solver=SolverConfig(iterations=4))
+    p = st.RodParams(radius=1.5e-3, stretch_modulus=1e6, bend_modulus=1e5,
+                     shear_modulus=5e4, penalty_stiffness=2.0,
+                     damping_translational=1e-4, damping_rotational=1e-7)
+    for r in range(rods):
+        w.add_rod(st.init_rod(n, 0.2, axis=(1.0, 0.0, 0.0),
+                              origin=(-0.1, 0.004 + 0.004 * r, 0.0)), p)
+    w.finalize()
+    if bindings == "one_way":
+        w.add_bindings(0, 1, BIND_ONE_WAY, stride=4)
+    elif bindings == "overlap":   # two couplings sharing points: ordered
+        w.add_bindings(0, 1, BIND_ONE_WAY, stride=4)
+        w.add_bindings(0, 1, BIND_BIDIRECTIONAL, stride=6)
+    for r in range(rods):
+        w.clamp_point(r, 0)
+    return w
+
+
+@pytest.mark.parametrize("mode", ["one_way", "overlap"])
+def test_bindings_bitwise(mode):
+    parity(lambda: _scene(mode), 200, 40)
+
+
+def test_grabs_drivers_and_commands_bitwise():
+    def script(world, stepper_run):
+        world.set_driver(0)
+        world.driver_velocity[0] = (0.0, 0.0, 0.02)
+        world.driver_rotation[0] = 3.0
+        stepper_run(20)
+        world.grab(0, 20, (0.0, 0.05, 0.0))
+        world.grab(1, 10, (0.02, 0.0, 0.01))
+        stepper_run(20)
+        world.release(0, 20)
+        stepper_run(10)
+
+    g, r = _scene(n=32), _scene(n=32)
+    with Engine(g) as eng:
+        script(g, eng.run_epoch)
+    # the oracle binds the world's arrays by pointer, so host edits between
+    # runs are seen, as with the reference core
+    script(r, OracleStepper(r).run)
+    assert_bitwise(g, r)
+
+
+def test_engine_commands_apply_at_epoch_boundaries():
+    w = _scene(n=16, rods=1)
+    w.set_driver(0)
+    with Engine(w) as eng:
+        t1 = eng.post_command("insert_velocity", value=0.05)
+        eng.run_epoch(10)
+        t2 = eng.post_command("grab", index=8, target=(0.0, 0.05, 0.0))
+        eng.run_epoch(10)
+        t3 = eng.post_command("release", index=8)
+        eng.run_epoch(5)
+        assert (t1.wait(1.0), t2.wait(1.0), t3.wait(1.0)) == (0, 10, 20)
+        assert [(s, c.name) for s, c in eng.command_log] == [
+            (0, "insert_velocity"), (10, "grab"), (20, "release")]
+        snap = eng.read_snapshot()
+    assert snap.step_index == 25 and snap.sequence % 2 == 0
+    assert np.array_equal(snap.positions, w.positions)
+    assert np.allclose(w.driver_velocity[0], [0.0, 0.0, 0.05])
+    assert not w.grab_active.any()
+
+
+def test_error_step_surfaces_as_floating_point_error():
+    w = _scene(n=12, rods=1)
+    with Engine(w) as eng:
+        eng.run_epoch(2)
+        w.positions[5] = np.nan
+        with pytest.raises(FloatingPointError, match="non-finite"):
+            eng.run_epoch(3)
+
+
+def test_rest_state_is_a_fixed_point():
+    w = World(dt=1e-4, gravity=(0.0, 0.0, 0.0))
+    w.add_rod(st.init_rod(32, 0.4), st.RodParams())
+    w.finalize()
+    p0, q0 = w.positions.copy(), w.frames.copy()
+    with Engine(w) as eng:
+        eng.run_epoch(1000)
+    assert np.max(np.abs(w.positions - p0)) <= 1e-12
+    assert np.max(np.abs(w.frames - q0)) <= 1e-12
+
+
+# -- fp32 mode: stated tolerance ----------------------------------------------
+
+@pytest.mark.parametrize("make,steps", [(wl.cantilever, 1000),
+                                         (wl.extensible, 1000),
+                                         (lambda: wl.hair(8), 1000)])
+def test_fp32_within_tolerance(make, steps):
+    g, r = make(), make()
+    run_gpu(g, steps, 100, precision="f32")
+    OracleStepper(r).run(steps)
+    L = max(np.ptp(r.positions, axis=0).max(), 1e-3)
+    dr = np.max(np.abs(g.positions - r.positions))
+    dq = np.max(np.abs(g.frames - r.frames))
+    assert dr <= 1e-5 * L, (dr, L)
+    assert dq <= 1e-4, dq
+
+
+def test_fp32_pair_short_horizon():
+    g, r = wl.pair(), wl.pair()
+    run_gpu(g, 10, 10, precision="f32")
+    OracleStepper(r).run(10)
+    dr = np.max(np.abs(g.positions - r.positions)) / np.max(np.abs(r.positions))
+    assert dr <= 1e-5, dr
+
+
+def test_fp64_fast_mode_within_1e9():
+    g, r = wl.cantilever(), wl.cantilever()
+    run_gpu(g, 1000, 100, precision="f64_fast")
+    OracleStepper(r).run(1000)
+    rel = np.max(np.abs(g.positions - r.positions)) / np.max(np.abs(r.positions))
+    assert rel <= 1e-9, rel
