@@ -94,6 +94,8 @@ struct StepArgs {
     int32_t has_fext;
     int32_t ncta;
     int32_t debug;                                 // bit 0: poison smem (NaN) first
+    int32_t any_binds;                             // launch has bindings (cluster/grid:
+    int32_t any_grabs;                             //   barrier count must be uniform)
     Real dt, beta, gx, gy, gz;
 };
 

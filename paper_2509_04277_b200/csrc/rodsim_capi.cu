@@ -747,6 +747,10 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.has_fext = h->has_fext;
     a.ncta = g.ncta;
     a.debug = h->debug;
+    for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
+        a.any_binds |= h->h_tasks[t].bind_count > 0;
+        a.any_grabs |= h->h_tasks[t].grab_count > 0;
+    }
     a.dt = Real(h->d.dt);
     a.beta = Real(h->d.beta);
     a.gx = Real(h->d.gx);

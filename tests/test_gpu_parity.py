@@ -116,6 +116,23 @@ def test_forced_cluster_pair_with_bindings_bitwise():
     parity(lambda: wl.pair(100, 0.2), 100, 10, force_tier=1, force_ctas=4)
 
 
+@pytest.mark.parametrize("tier,ctas", [(1, 4), (2, 3)])
+def test_forced_multi_cta_tiers_with_grab_bitwise(tier, ctas):
+    def make():
+        w = wl.cantilever(120, 0.3)
+        w.grab(0, 100, (0.2, 0.05, 0.01))
+        return w
+    parity(make, 80, 20, force_tier=tier, force_ctas=ctas)
+
+
+def test_cluster_pair_overlapping_bindings_sequential_bitwise():
+    def make():
+        w = wl.pair(100, 0.2)
+        w.add_bindings(0, 1, BIND_ONE_WAY, stride=5)
+        return w
+    parity(make, 60, 20, force_tier=1, force_ctas=3)
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_cta_variants_bitwise(variant):
     parity(lambda: wl.cantilever(100, 0.2), 100, 50, force_variant=variant)
