@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""Benchmark: CoRdE rod step on B200 (BASELINE.json metric).
+
+Headline line (one JSON line on rank 0):
+  metric  BASELINE.json's metric; value = batched element-steps/s of cfg5
+          (65536 hair rods x 128 elements, fp64 mirror mode, K physics steps
+          per launch), whole job over N GPUs, rods sharded across ranks
+          (strong scaling: the 65536-rod batch is fixed), device-resident
+          state, CUDA events on the launching stream, max over ranks.
+  e2e     the same metric through Engine.run_epoch with the World's host
+          numpy arrays: H2D of the state every step, D2H of the result.
+  single_rod  (N == 1) µs per time step vs element count for one rod
+          (cfg1, cfg2, cfg3 pair incl. the 1 kHz haptic frame loop, cfg4
+          sweep) with the reference CPU core timed beside it.
+  roofline    dominant kernel, HBM bytes against MEASURED_PEAKS.json.
+  cpu_baseline  the reference's own compiled core (oracle/_ref) or the C
+          restatement, on the box's host cores, bounded sample.
+
+`--impl reference` times the reference CPU implementation on the same
+metric/config (rank 0 only; other ranks exit).
+"""
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = ("µs/time-step vs #elements (1 rod); element-steps/s batched at "
+          "1/2/4/8 GPUs")
+TOTAL_RODS = 65536
+ELEMENTS = 128
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32", "f64_fast"])
+    ap.add_argument("--rods", type=int, default=TOTAL_RODS)
+    ap.add_argument("--k", type=int, default=1, help="physics steps per launch")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-single", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-variant", type=int, default=-1)
+    return ap.parse_args()
+
+
+# ---- algorithmic bytes -----------------------------------
+
+def algorithmic_bytes_per_rod(points, elems, real_bytes=8):
+    """pos, vel, q, w read + written once per launch; rest + u* read once."""
+    return real_bytes * (2 * (6 * points + 7 * elems) + 4 * elems)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(key):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(key)
+    except Exception:
+        return None
+
+
+# ---- clocks sampled during the timed region --------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- CPU baseline: the reference core on host cores -------------------------
+
+def _cpu_worker(args):
+    rods, first, steps, kind = args
+    sys.path.insert(0, ROOT)
+    from oracle.oracle import OracleStepper, ReferenceStepper
+    from paper_2509_04277_b200 import workloads
+    w = workloads.hair(rods, ELEMENTS, first=first)
+    stepper = ReferenceStepper(w) if kind == "reference" else OracleStepper(w)
+    stepper.run(1)   # warm-up
+    t0 = time.perf_counter()
+    stepper.run(steps)
+    dt = time.perf_counter() - t0
+    return rods * ELEMENTS * steps, dt
+
+
+def cpu_kind():
+    from oracle.oracle import reference_core_path
+    return "reference" if reference_core_path() else "port"
+
+
+def cpu_baseline(procs, rods_per_proc=192, steps=20, repeats=1):
+    """Element-steps/s of the reference CPU path on `procs` processes (one
+    World shard per process, Engine(backend="serial") semantics)."""
+    kind = cpu_kind()
+    ctx = mp.get_context("fork")
+    best = 0.0
+    with ctx.Pool(procs) as pool:
+        for _ in range(repeats):
+            out = pool.map(_cpu_worker, [(rods_per_proc, i * rods_per_proc, steps, kind)
+                                         for i in range(procs)])
+            best = max(best, sum(n / t for n, t in out))
+    return {"value": best, "unit": "element-steps/s", "cores": procs, "kind": kind,
+            "sample": f"hair {rods_per_proc} rods x {ELEMENTS} el x {steps} steps "
+                      f"per process, {procs} processes (best of {repeats})"}
+
+
+def cpu_single_rod_us(make, steps):
+    from oracle.oracle import OracleStepper, ReferenceStepper
+    kind = cpu_kind()
+    w = make()
+    s = ReferenceStepper(w) if kind == "reference" else OracleStepper(w)
+    s.run(2)
+    t0 = time.perf_counter()
+    s.run(steps)
+    return (time.perf_counter() - t0) / steps * 1e6, kind
+
+
+# ---- distributed plumbing ---------------------------------------------------
+
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class Dist:
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local = world, rank, local
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.dist = dist
+            self.torch = torch
+            self.pg = True
+
+    def barrier(self):
+        if self.pg:
+            self.dist.barrier()
+
+    def max(self, x):
+        if not self.pg:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.dist.destroy_process_group()
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device buffer owned by the library."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape,
+                                         "typestr": typestr, "version": 3}
+
+
+# ---- single-rod latency measurements (rank 0, N = 1) ------------------------
+
+def single_rod_suite(precision):
+    from paper_2509_04277_b200 import workloads as wl
+    from paper_2509_04277_b200.engine import Engine
+
+    def device_us(make, k, launches):
+        w = make()
+        with Engine(w, precision=precision) as eng:
+            dev = eng.device_world
+            dev.run(k)
+            dev.synchronize()
+            dev.timer_start()
+            for _ in range(launches):
+                dev.run(k)
+            dev.timer_stop()
+            ms = dev.timer_ms()
+            plan = eng.plan()["groups"][0]
+        return ms * 1e3 / (k * launches), plan
+
+    out = {}
+    us, plan = device_us(wl.cantilever, 1000, 3)
+    cpu, kind = cpu_single_rod_us(wl.cantilever, 1000)
+    out["cfg1_cantilever_64"] = {"us_per_step": us, "k": 1000, "tier": plan["tier"],
+                                 "cpu_us_per_step": cpu, "cpu_kind": kind}
+    us, plan = device_us(wl.extensible, 10, 100)
+    cpu, _ = cpu_single_rod_us(wl.extensible, 200)
+    out["cfg2_extensible_512"] = {"us_per_step": us, "k": 10, "tier": plan["tier"],
+                                  "cpu_us_per_step": cpu}
+    us, plan = device_us(wl.pair, 10, 100)
+    cpu, _ = cpu_single_rod_us(wl.pair, 100)
+    # haptic frame loop: commands in, K = 10 steps (1 ms simulated), state out
+    w = wl.pair()
+    frames = []
+    with Engine(w, precision=precision) as eng:
+        for i in range(1100):
+            t0 = time.perf_counter()
+            eng.post_command("insert_velocity", rod=0, value=0.05 + 1e-4 * (i % 7),
+                             axis=(0.0, 0.0, 1.0))
+            eng.run_epoch(10)
+            tip = w.positions[w.rod_infos[0].point_offset + w.rod_infos[0].num_points - 1]
+            frames.append(time.perf_counter() - t0)
+            _ = float(tip[2])
+    frames = np.array(frames[100:]) * 1e6
+    out["cfg3_pair_2x512"] = {
+        "us_per_step": us, "k": 10, "tier": plan["tier"], "steps_per_s": 1e6 / us,
+        "cpu_us_per_step": cpu,
+        "haptic_frame_us": {"median": float(np.median(frames)),
+                            "p99": float(np.percentile(frames, 99)),
+                            "frames": int(frames.size),
+                            "rate_hz_median": float(1e6 / np.median(frames))}}
+    sweep = {}
+    for n in (16, 64, 256, 1024, 4096, 16384):
+        row = {}
+        for k in (1, 10, 100):
+            launches = max(2, min(200, 2000 // k))
+            us, plan = device_us(lambda: wl.sweep(n), k, launches)
+            row[f"k{k}"] = us
+        row["tier"] = plan["tier"]
+        row["ctas"] = plan["ctas"]
+        row["cpu_us_per_step"], _ = cpu_single_rod_us(lambda: wl.sweep(n),
+                                                      max(3, 20000 // n))
+        sweep[str(n)] = row
+    out["cfg4_sweep_us_per_step"] = sweep
+    return out
+
+
+# ---- arms ---------------------------------------------------------------------
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    kind = cpu_kind()
+    ctx = mp.get_context("fork")
+    rods_pp, steps_pp = 128, 10
+    vals = []
+    with ctx.Pool(procs) as pool:
+        jobs = [(rods_pp, i * rods_pp, steps_pp, kind) for i in range(procs)]
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker, jobs)
+        t_all = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            out = pool.map(_cpu_worker, jobs)
+            t_all.append(time.perf_counter() - t0)
+            vals.append(sum(n / t for n, t in out))
+    value = float(np.median(vals))
+    sample = (f"hair {rods_pp} rods x {ELEMENTS} el x {steps_pp} steps per process, "
+              f"{procs} processes; element-steps/s summed over processes")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value,
+        "unit": "element-steps/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(np.median(t_all)) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg5 hair: 65536 rods x 128 elements (bounded CPU "
+                               "sample of the same rods)",
+                   "rods": TOTAL_RODS, "elements_per_rod": ELEMENTS,
+                   "iterations": 10, "dt": 1e-4},
+        "cpu_baseline": {"value": value, "unit": "element-steps/s", "cores": procs,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "element-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    world, rank, local = dist_env()
+    D = Dist(world, rank, local)
+    from paper_2509_04277_b200 import workloads as wl
+    from paper_2509_04277_b200._lib import RS_STATE
+    from paper_2509_04277_b200.engine import Engine
+
+    first, per = wl.shard(args.rods, world, rank)
+    t_build = time.perf_counter()
+    w = wl.hair(per, ELEMENTS, first=first)
+    t_build = time.perf_counter() - t_build
+    eng = Engine(w, precision=args.precision, device=local,
+                 force_variant=args.force_variant)
+    dev = eng.device_world
+    plan = eng.plan()
+    P, E = w.num_points, w.num_elements
+    real = 4 if args.precision == "f32" else 8
+
+    # ---- device-resident timed region --------------------------------
+    for _ in range(args.warmup):
+        dev.run(args.k)
+    dev.synchronize()
+    D.barrier()
+    launches0 = dev.launch_count()
+    with ClockSampler(local) as clk:
+        dev.timer_start()
+        for _ in range(args.steps):
+            dev.run(args.k)
+        dev.timer_stop()
+        ms = dev.timer_ms()
+    dev.synchronize()
+    D.barrier()
+    launches = dev.launch_count() - launches0
+    ms_max = D.max(ms)
+    elem_steps = args.rods * ELEMENTS * args.k * args.steps
+    value = elem_steps / (ms_max * 1e-3)
+
+    # roofline: dominant (only) kernel, algorithmic bytes per launch
+    launch_ms = ms / max(launches, 1)
+    bytes_per_launch = per * algorithmic_bytes_per_rod(ELEMENTS + 1, ELEMENTS, real)
+    peak, peak_src = load_peaks()
+    achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
+    traffic = load_traffic(f"hair_{args.precision}_k{args.k}_r{per}")
+
+    # ---- e2e through the public API (host numpy arrays) --------------
+    state_bytes = 8 * (6 * P + 7 * E)
+    control_bytes = w.driver_velocity.nbytes + w.driver_rotation.nbytes + \
+        w.grab_target.nbytes + w.grab_point.nbytes + w.grab_active.nbytes
+    eng.run_epoch(args.k)
+    D.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        eng.run_epoch(args.k)
+    e2e_s = time.perf_counter() - t0
+    e2e_max = D.max(e2e_s)
+    e2e_value = args.rods * ELEMENTS * args.k * args.e2e_steps / e2e_max
+
+    # ---- NCCL gather of the final positions (results only) -----------
+    gathered = None
+    if world > 1:
+        import torch
+        ptr = dev.device_ptr(0)
+        src = torch.as_tensor(_CudaArray(ptr, (P * 3,), "<f8" if real == 8 else "<f4"),
+                              device=f"cuda:{local}")
+        out = torch.empty(world * P * 3, dtype=src.dtype, device=f"cuda:{local}")
+        D.dist.all_gather_into_tensor(out, src.contiguous())
+        torch.cuda.synchronize()
+        gathered = int(out.numel())
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "element-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": {"f64": "f64", "f32": "f32", "f64_fast": "f64"}[args.precision],
+            "data": "synthetic",
+            "config": {"workload": "cfg5 hair: 65536 rods x 128 elements, roots "
+                                   "clamped, sharded over ranks",
+                       "rods": args.rods, "rods_per_gpu": per,
+                       "elements_per_rod": ELEMENTS, "steps_per_launch": args.k,
+                       "iterations": 10, "dt": 1e-4,
+                       "parity_mode": args.precision,
+                       "l2": "inputs larger than L2 (state %.0f MB/GPU)" % (state_bytes / 1e6),
+                       "plan": plan["groups"]},
+            "e2e": {"value": e2e_value, "unit": "element-steps/s",
+                    "h2d_bytes_per_step": state_bytes + control_bytes,
+                    "d2h_bytes_per_step": state_bytes,
+                    "steps": args.e2e_steps, "api": "Engine.run_epoch"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "bytes_per_launch": bytes_per_launch,
+                         "launch_ms": launch_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "build_s": t_build,
+        }
+        if gathered is not None:
+            line["nccl_gather_elems"] = gathered
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
+        if world == 1 and not args.no_single:
+            line["single_rod"] = single_rod_suite(args.precision)
+        print(json.dumps(line))
+    eng.close()
+    D.close()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

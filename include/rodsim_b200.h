@@ -120,10 +120,18 @@ const char *rs_last_error(void);
  * launching stream; returns milliseconds of the last epoch's launches. */
 int rs_enable_timing(rs_handle h, int on);
 double rs_last_kernel_ms(rs_handle h);
+/* CUDA events on the launching stream around any span of epochs:
+ * rs_timer_start, rs_run_epoch..., rs_timer_stop, rs_timer_ms (syncs). */
+int rs_timer_start(rs_handle h);
+int rs_timer_stop(rs_handle h);
+double rs_timer_ms(rs_handle h);
 /* Number of kernel launches issued so far. */
 int64_t rs_launch_count(rs_handle h);
 /* JSON description of the launch plan (tiers, CTAs, threads, variants). */
 int rs_plan_json(rs_handle h, char *buf, int64_t len);
+/* The same plan computed without a device (no CUDA calls, no occupancy
+ * checks) for a device with `num_sms` SMs: host-logic tests on CPU. */
+int rs_plan_dry(const rs_world_desc *desc, int32_t num_sms, char *buf, int64_t len);
 /* Raw device pointer of a state array: 0 pos, 1 vel, 2 q, 3 w (element
  * type double for RS_F64_*, float for RS_F32). */
 int rs_device_ptr(rs_handle h, int32_t which, void **out);
@@ -131,6 +139,9 @@ int rs_device_ptr(rs_handle h, int32_t which, void **out);
  * pairs, computed on the device with the fp64 mirror build flags. */
 int rs_selftest_div(const double *a, const double *b, int64_t n, double *q_ieee,
                     double *q_fast);
+/* Measured issue rate of one pipe on the current device (operations/s):
+ * kind 0 DFMA, 1 DADD, 2 DMUL, 3 FFMA.  Compute cross-check for the bench. */
+int rs_pipe_peak(int kind, double *ops_per_s);
 
 #ifdef __cplusplus
 }

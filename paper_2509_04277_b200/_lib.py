@@ -81,7 +81,20 @@ SIGNATURES = [
     ("rs_plan_json", _i32, [_p, ctypes.c_char_p, _i64]),
     ("rs_device_ptr", _i32, [_p, _i32, ctypes.POINTER(_p)]),
     ("rs_selftest_div", _i32, [_p, _p, _i64, _p, _p]),
+    ("rs_timer_start", _i32, [_p]),
+    ("rs_timer_stop", _i32, [_p]),
+    ("rs_timer_ms", _f64, [_p]),
+    ("rs_pipe_peak", _i32, [_i32, ctypes.POINTER(_f64)]),
+    ("rs_plan_dry", _i32, [ctypes.POINTER(WorldDesc), _i32, ctypes.c_char_p, _i64]),
 ]
+
+
+def pipe_peak(kind):
+    """Measured ops/s of one pipe: 0 DFMA, 1 DADD, 2 DMUL, 3 FFMA."""
+    lib = load_library()
+    out = _f64(0.0)
+    check(lib.rs_pipe_peak(int(kind), ctypes.byref(out)), lib)
+    return out.value
 
 _LIB = None
 
@@ -126,6 +139,71 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
+def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
+               force_variant=-1):
+    """`rs_world_desc` over the World's arrays (bound by pointer, like
+    make_context, _core.pyx:219-403) plus the dict keeping them alive."""
+    w = world
+    c = np.ascontiguousarray
+    offs = np.array([i.point_offset for i in w.rod_infos] + [w.num_points],
+                    dtype=np.int64)
+    arrays = {
+        "rod_offsets": offs,
+        "pos": w.positions, "vel": w.velocities, "q": w.frames,
+        "w": w.angular_velocities,
+        "rest": c(w.rest_lengths), "ustar": c(w.intrinsic_strains),
+        "mass": c(w.masses), "invm": c(w.inv_masses),
+        "inert": c(w.inertias), "fext": c(w.external_forces),
+        "ks": c(w.stretch_k), "kp": c(w.penalty_k), "gt": c(w.gamma_t),
+        "gr": c(w.gamma_r), "ext": c(w.extensible), "kb": c(w.bend_k),
+        "plock": c(w.point_locked).view(np.uint8),
+        "flock": c(w.frame_locked).view(np.uint8),
+        "jvalid": c(w.junction_valid).view(np.uint8),
+        "elem_point": c(w.elem_point, dtype=np.int64),
+        "elem_parity": c(w.elem_parity, dtype=np.int64),
+        "drv_pt": c(w.driven_point, dtype=np.int64),
+        "drv_fr": c(w.driven_frame, dtype=np.int64),
+        "bind_a": c(w.bind_a, dtype=np.int64),
+        "bind_b": c(w.bind_b, dtype=np.int64),
+        "bind_mode": c(w.bind_mode, dtype=np.int64),
+        "drv_v": w.driver_velocity, "drv_rot": w.driver_rotation,
+        "g_act": w.grab_active, "g_pt": w.grab_point, "g_tgt": w.grab_target,
+    }
+    for k in ("pos", "vel", "q", "w", "drv_v", "drv_rot", "g_act", "g_pt", "g_tgt"):
+        a = arrays[k]
+        if not (a.flags.c_contiguous and a.flags.writeable):
+            raise ValueError(f"world array {k} must be C-contiguous and writeable")
+    d = WorldDesc()
+    d.abi_version = RS_ABI_VERSION
+    d.precision = PRECISIONS[precision]
+    d.device = device
+    d.force_tier = force_tier
+    d.force_ctas = force_ctas
+    d.force_variant = force_variant
+    d.P, d.E, d.R = w.num_points, w.num_elements, len(w.rod_infos)
+    d.iters = w.solver.iterations
+    d.step_index = w.step_index
+    d.dt = w.dt
+    d.beta = w.solver.position_bias
+    d.gx, d.gy, d.gz = (float(x) for x in w.gravity)
+    for name, arr in arrays.items():
+        setattr(d, name, _ptr(arr))
+    d.nbind = arrays["bind_a"].shape[0]
+    d.ngrab = arrays["g_act"].shape[0]
+    return d, arrays
+
+
+def plan_dry(world, num_sms=148, precision="f64", **force):
+    """Launch plan for `world` without a device (rs_plan_dry)."""
+    lib = load_library()
+    d, keep = build_desc(world, precision, 0, force.get("force_tier", -1),
+                         force.get("force_ctas", 0), force.get("force_variant", -1))
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(lib.rs_plan_dry(ctypes.byref(d), int(num_sms), buf, len(buf)), lib)
+    del keep
+    return json.loads(buf.value.decode())
+
+
 class DeviceWorld:
     """One device mirror of a World (a C handle) plus the arrays it binds.
 
@@ -138,56 +216,9 @@ class DeviceWorld:
         self.lib = load_library()
         self.world = world
         self.precision = precision
-        w = world
-        c = np.ascontiguousarray
-        offs = np.array([i.point_offset for i in w.rod_infos]
-                        + [w.num_points], dtype=np.int64)
-        self.arrays = {
-            "rod_offsets": offs,
-            "pos": w.positions, "vel": w.velocities, "q": w.frames,
-            "w": w.angular_velocities,
-            "rest": c(w.rest_lengths), "ustar": c(w.intrinsic_strains),
-            "mass": c(w.masses), "invm": c(w.inv_masses),
-            "inert": c(w.inertias), "fext": c(w.external_forces),
-            "ks": c(w.stretch_k), "kp": c(w.penalty_k), "gt": c(w.gamma_t),
-            "gr": c(w.gamma_r), "ext": c(w.extensible), "kb": c(w.bend_k),
-            "plock": c(w.point_locked).view(np.uint8),
-            "flock": c(w.frame_locked).view(np.uint8),
-            "jvalid": c(w.junction_valid).view(np.uint8),
-            "elem_point": c(w.elem_point, dtype=np.int64),
-            "elem_parity": c(w.elem_parity, dtype=np.int64),
-            "drv_pt": c(w.driven_point, dtype=np.int64),
-            "drv_fr": c(w.driven_frame, dtype=np.int64),
-            "bind_a": c(w.bind_a, dtype=np.int64),
-            "bind_b": c(w.bind_b, dtype=np.int64),
-            "bind_mode": c(w.bind_mode, dtype=np.int64),
-            "drv_v": w.driver_velocity, "drv_rot": w.driver_rotation,
-            "g_act": w.grab_active, "g_pt": w.grab_point,
-            "g_tgt": w.grab_target,
-        }
-        for k in ("pos", "vel", "q", "w", "drv_v", "drv_rot", "g_act",
-                  "g_pt", "g_tgt"):
-            a = self.arrays[k]
-            if not (a.flags.c_contiguous and a.flags.writeable):
-                raise ValueError(f"world array {k} must be C-contiguous and writeable")
-        d = WorldDesc()
-        d.abi_version = RS_ABI_VERSION
-        d.precision = PRECISIONS[precision]
-        d.device = device
-        d.force_tier = force_tier
-        d.force_ctas = force_ctas
-        d.force_variant = force_variant
-        d.P, d.E, d.R = w.num_points, w.num_elements, len(w.rod_infos)
-        d.iters = w.solver.iterations
-        d.step_index = w.step_index
-        d.dt = w.dt
-        d.beta = w.solver.position_bias
-        d.gx, d.gy, d.gz = (float(x) for x in w.gravity)
-        for name, arr in self.arrays.items():
-            setattr(d, name, _ptr(arr))
-        d.nbind = self.arrays["bind_a"].shape[0]
-        d.ngrab = self.arrays["g_act"].shape[0]
-        self.desc = d
+        self.desc, self.arrays = build_desc(world, precision, device, force_tier,
+                                            force_ctas, force_variant)
+        d = self.desc
         h = _p()
         check(self.lib.rs_create(ctypes.byref(d), ctypes.byref(h)), self.lib)
         self.handle = h
@@ -251,6 +282,15 @@ class DeviceWorld:
 
     def launch_count(self):
         return int(self.lib.rs_launch_count(self.handle))
+
+    def timer_start(self):
+        check(self.lib.rs_timer_start(self.handle), self.lib)
+
+    def timer_stop(self):
+        check(self.lib.rs_timer_stop(self.handle), self.lib)
+
+    def timer_ms(self):
+        return float(self.lib.rs_timer_ms(self.handle))
 
     def plan(self):
         buf = ctypes.create_string_buffer(1 << 16)

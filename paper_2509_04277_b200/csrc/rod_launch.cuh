@@ -25,6 +25,11 @@ static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
     auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
+    // all of the unified L1/shared array as shared memory: several CTAs
+    // (rods) per SM are what hides latency in the batched case
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             int(cudaSharedmemCarveoutMaxShared));
+    if (e != cudaSuccess) return e;
     if constexpr (TIER == TIER_CLUSTER) {
         if (cluster > 8) {
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -56,6 +61,9 @@ template <typename Real, int S, int CAP, int TIER, bool UNI>
 static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out) {
     auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             int(cudaSharedmemCarveoutMaxShared));
     if (e != cudaSuccess) return e;
     if constexpr (TIER == TIER_CLUSTER) {
         if (cluster > 8) {
@@ -102,6 +110,7 @@ static cudaError_t dispatch(int what, int variant, int tier, bool uni, const Ste
             case 2: return RSB_D(2, 512, TIER_CTA);
             case 3: return RSB_D(2, 768, TIER_CTA);
             case 4: return RSB_D(3, 1152, TIER_CTA);
+            case 5: return RSB_D(1, 160, TIER_CTA);
         }
     } else if (tier == TIER_CLUSTER) {
         switch (variant) {

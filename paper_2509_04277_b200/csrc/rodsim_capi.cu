@@ -67,8 +67,11 @@ int fail(int code, const char* fmt, ...) {
 struct Variant {
     int S, CAP;
 };
-constexpr Variant kVariants[] = {{1, 128}, {1, 256}, {2, 512}, {2, 768}, {3, 1152}};
-constexpr int kNumVariants = 5;
+// capacity-ordered variants 0..4, then the occupancy-tuned batched variant 5
+constexpr Variant kVariants[] = {{1, 128}, {1, 256}, {2, 512}, {2, 768}, {3, 1152}, {1, 160}};
+constexpr int kNumVariants = 6;
+constexpr int kNumCapVariants = 5;
+constexpr int kBatchVariant = 5;
 constexpr int kClusterVariant = 4;
 constexpr int kMaxCluster = 16;
 constexpr int kRingCap = 64;
@@ -105,13 +108,15 @@ struct rs_handle_s {
     int prec = RS_F64_MIRROR;
     size_t rsz = 8;                 // sizeof(Real) on the device
     cudaStream_t st = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // per-epoch kernel timing
+    cudaEvent_t tm0 = nullptr, tm1 = nullptr;   // caller-bracketed spans
     bool timing = false;
     bool timed = false;
     double last_ms = 0.0;
     int64_t launches = 0;
     int num_sms = 0;
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
+    bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
 
     // device mirrors
     DevBuf pos, vel, q, w;
@@ -325,7 +330,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     }
 
     // -- choose tiers --------------------------------------------------------
-    const int cta_cap = kVariants[kNumVariants - 1].CAP;
+    const int cta_cap = kVariants[kNumCapVariants - 1].CAP;
     std::vector<int> seg_tier(segs.size());
     int64_t max_cta_seg = 0;
     for (size_t i = 0; i < segs.size(); ++i) {
@@ -367,6 +372,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     if (max_cta_seg > 0) {
         int v = 0;
         while (kVariants[v].CAP < max_cta_seg) ++v;
+        // batches of short rods: one rod per 160-thread CTA, 4 CTAs per SM
+        int64_t cta_points = 0;
+        for (size_t i = 0; i < segs.size(); ++i)
+            if (seg_tier[i] == TIER_CTA) cta_points += segs[i].p1 - segs[i].p0;
+        if (max_cta_seg <= kVariants[kBatchVariant].CAP &&
+            cta_points >= int64_t(2) * kVariants[kBatchVariant].CAP * h->num_sms)
+            v = kBatchVariant;
         if (d.force_variant >= 0) {
             if (d.force_variant >= kNumVariants || kVariants[d.force_variant].CAP < max_cta_seg)
                 return fail(RS_E_INVALID, "force_variant %d cannot hold %lld points", d.force_variant,
@@ -544,7 +556,8 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         g.threads = std::max(g.threads, 32);
         size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap).total
                                         : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap).total;
-        if (smem > kMaxSmem && g.bind_cap > 0) {
+        const int stage_cap = SCRATCH_FIELDS * var.CAP / BIND_REALS;
+        if ((smem > kMaxSmem || g.bind_cap > stage_cap) && g.bind_cap > 0) {
             // no room to stage binding constants: apply bindings in order
             for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
                 CtaTask& tk = h->h_tasks[t];
@@ -559,6 +572,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         }
         if (smem > kMaxSmem) return fail(RS_E_UNSUPPORTED, "shared memory plan %zu B too large", smem);
         g.smem = smem;
+        if (h->dry) continue;
         int occ = 0;
         int rc = occupancy_query(h, g.variant, g.tier, g.uni, g.threads, g.smem, g.cluster, &occ);
         if (rc) return rc;
@@ -823,6 +837,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
         return bail(fail(RS_E_CUDA, "device query failed"));
     if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess ||
+        cudaEventCreate(&h->tm0) != cudaSuccess || cudaEventCreate(&h->tm1) != cudaSuccess ||
         cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMallocHost(&h->h_err, sizeof(unsigned long long)) != cudaSuccess)
         return bail(fail(RS_E_CUDA, "CUDA resource creation failed"));
@@ -986,6 +1001,8 @@ void rs_destroy(rs_handle h) {
     if (h->stage) cudaFreeHost(h->stage);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->tm0) cudaEventDestroy(h->tm0);
+    if (h->tm1) cudaEventDestroy(h->tm1);
     if (h->st) cudaStreamDestroy(h->st);
     delete h;
 }
@@ -1003,6 +1020,26 @@ double rs_last_kernel_ms(rs_handle h) {
 }
 
 int64_t rs_launch_count(rs_handle h) { return h ? h->launches : -1; }
+
+int rs_timer_start(rs_handle h) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    CK(cudaEventRecord(h->tm0, h->st));
+    return RS_OK;
+}
+
+int rs_timer_stop(rs_handle h) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    CK(cudaEventRecord(h->tm1, h->st));
+    return RS_OK;
+}
+
+double rs_timer_ms(rs_handle h) {
+    if (!h) return -1.0;
+    if (cudaEventSynchronize(h->tm1) != cudaSuccess) return -1.0;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h->tm0, h->tm1) != cudaSuccess) return -1.0;
+    return ms;
+}
 
 int rs_plan_json(rs_handle h, char* buf, int64_t len) {
     if (!h || !buf || len <= 0) return fail(RS_E_INVALID, "bad argument");
@@ -1028,6 +1065,23 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
     return RS_OK;
 }
 
+int rs_plan_dry(const rs_world_desc* desc, int32_t num_sms, char* buf, int64_t len) {
+    if (!desc) return fail(RS_E_INVALID, "null argument");
+    if (desc->P < 2 || desc->R < 1 || desc->E != desc->P - desc->R)
+        return fail(RS_E_INVALID, "inconsistent world sizes");
+    rs_handle_s h;
+    h.d = *desc;
+    h.prec = desc->precision;
+    h.rsz = h.prec == RS_F32 ? sizeof(float) : sizeof(double);
+    h.num_sms = num_sms;
+    h.dry = true;
+    std::vector<uint32_t> pflags;
+    std::vector<int32_t> pt_elem;
+    int rc = plan(&h, pflags, pt_elem);
+    if (rc) return rc;
+    return rs_plan_json(&h, buf, len);
+}
+
 int rs_device_ptr(rs_handle h, int32_t which, void** out) {
     if (!h || !out) return fail(RS_E_INVALID, "null argument");
     const DevBuf* b[] = {&h->pos, &h->vel, &h->q, &h->w};
@@ -1043,6 +1097,23 @@ namespace mirror {
 cudaError_t div_selftest(const double*, const double*, int64_t, double*, double*);
 }
 }  // namespace rsb
+
+namespace rsb {
+namespace fast {
+cudaError_t pipe_peak(int kind, int blocks, int threads, int iters, float* ms, double* ops);
+}
+}  // namespace rsb
+
+extern "C" int rs_pipe_peak(int kind, double* ops_per_s) {
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    float ms = 0.f;
+    double ops = 0.0;
+    CK(rsb::fast::pipe_peak(kind, sms * 8, 256, 4096, &ms, &ops));
+    *ops_per_s = ops / (double(ms) * 1e-3);
+    return RS_OK;
+}
 
 extern "C" int rs_selftest_div(const double* a, const double* b, int64_t n, double* q_ieee,
                                double* q_fast) {

@@ -184,6 +184,8 @@ class Engine:
         self._pending = []
         self._force = (force_tier, force_ctas, force_variant)
         self._lock = threading.Lock()
+        self._snapshot_readers = False
+        self._snapshot_stale = False
         self._dev = None
         self._bind()
         self.snapshot_buffer.publish(world)
@@ -317,7 +319,11 @@ class Engine:
             self.world.step_index += steps
             self._resolve_applied()
             self.last_contacts = contacts
-            self.snapshot_buffer.publish(self.world)
+            if self._small or self._snapshot_readers:
+                self.snapshot_buffer.publish(self.world)
+                self._snapshot_stale = False
+            else:   # large batches: publish on first read (saves a full copy)
+                self._snapshot_stale = True
             self._check_core_error()
             wall = time.perf_counter_ns() - t0
         return {"wall_ns": wall, "steps": steps,
@@ -341,6 +347,11 @@ class Engine:
         self._dev.update_params(self.world.dt, self.world.solver.iterations)
 
     def read_snapshot(self):
+        with self._lock:
+            self._snapshot_readers = True
+            if self._snapshot_stale:
+                self.snapshot_buffer.publish(self.world)
+                self._snapshot_stale = False
         return self.snapshot_buffer.read()
 
     # -- introspection -----------------------------------------------------

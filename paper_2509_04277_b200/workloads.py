@@ -103,5 +103,14 @@ def hair(rods, elements=128, length=0.4, first=0):
     return w
 
 
+def shard(total_rods, world_size, rank):
+    """(first rod, rod count) of `rank`'s slice of a batch: rods are
+    independent, so ranks step disjoint slices with no per-step exchange."""
+    if total_rods % world_size:
+        raise ValueError("rods must divide evenly across ranks")
+    per = total_rods // world_size
+    return rank * per, per
+
+
 BUILDERS = {"cantilever": cantilever, "extensible": extensible, "pair": pair,
             "sweep": sweep, "hair": hair}

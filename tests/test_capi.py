@@ -1,0 +1,137 @@
+"""The C ABI boundary (include/rodsim_b200.h) and the launch planner, on CPU.
+
+* every entry point the header declares is exported by librodsim_b200.so
+  and typed in _lib.SIGNATURES;
+* the ctypes mirror of `rs_world_desc` has the C compiler's layout;
+* the planner (rs_plan_dry: the same code path rs_create runs, minus device
+  queries) maps the BASELINE configs to the intended tiers;
+* without a device the engine fails loudly (there is no CPU fallback).
+"""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, have_gpu
+from paper_2509_04277_b200 import _lib
+from paper_2509_04277_b200 import state as st
+from paper_2509_04277_b200 import workloads as wl
+from paper_2509_04277_b200.world import BIND_BIDIRECTIONAL, World
+
+HEADER = os.path.join(ROOT, "include", "rodsim_b200.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^[a-z_0-9 ]+[ \*]+(rs_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_entry_point():
+    lib = _lib.load_library()
+    declared = header_functions()
+    assert len(declared) >= 20
+    typed = {name for name, _, _ in _lib.SIGNATURES}
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in typed, name
+
+
+def test_world_desc_layout_matches_c(tmp_path):
+    fields = [f for f, _ in _lib.WorldDesc._fields_]
+    src = tmp_path / "probe.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "rodsim_b200.h"\n'
+        "int main(void){printf(\"%zu\\n\", sizeof(rs_world_desc));\n"
+        + "".join(f'printf("%zu\\n", offsetof(rs_world_desc, {f}));\n' for f in fields)
+        + "return 0;}\n")
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    out = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert out[0] == ctypes.sizeof(_lib.WorldDesc)
+    for f, off in zip(fields, out[1:]):
+        assert getattr(_lib.WorldDesc, f).offset == off, f
+
+
+# -- planner ---------------------------------------------------------------------
+
+def plan(world, **kw):
+    return _lib.plan_dry(world, **kw)["groups"]
+
+
+def test_plan_single_rods_by_size():
+    g = plan(wl.cantilever())
+    assert len(g) == 1 and g[0]["tier"] == "cta" and g[0]["ctas"] == 1 and g[0]["uniform"]
+    assert plan(wl.extensible())[0]["tier"] == "cta"
+    g = plan(wl.sweep(4096))[0]
+    assert g["tier"] == "cluster" and 2 <= g["ctas"] <= 16 and g["cluster"] == g["ctas"]
+    g = plan(wl.sweep(16384))[0]
+    assert g["tier"] == "cluster" and g["ctas"] <= 16
+    g = plan(wl.sweep(32768))[0]
+    assert g["tier"] == "grid" and g["ctas"] > 16
+
+
+def test_plan_pair_keeps_bound_rods_together_with_parallel_bindings():
+    g = plan(wl.pair())
+    assert len(g) == 1 and g[0]["tier"] == "cta" and g[0]["points"] == 1026
+    assert g[0]["bind_cap"] == 513          # a matching: one binding per thread slot
+
+
+def test_plan_batched_rods_use_occupancy_variant():
+    g = plan(wl.hair(2048))[0]
+    assert g["tier"] == "cta" and g["variant"] == 5 and g["ctas"] == 2048
+    assert g["threads"] == 160
+
+
+def test_plan_forced_tiers_and_variants():
+    w = wl.cantilever(200, 0.4)
+    assert plan(w, force_tier=1, force_ctas=5)[0]["ctas"] == 5
+    assert plan(w, force_tier=2, force_ctas=3)[0]["tier"] == "grid"
+    assert plan(w, force_variant=4)[0]["variant"] == 4
+    with pytest.raises(ValueError):
+        plan(wl.cantilever(300, 0.6), force_variant=0)
+
+
+def test_plan_segments_span_bound_non_adjacent_rods():
+    w = World()
+    for n in (10, 20, 10):
+        w.add_rod(st.init_rod(n, 0.01 * n), st.RodParams())
+    w.finalize()
+    w.add_bindings(0, 2, BIND_BIDIRECTIONAL)
+    g = plan(w)
+    assert len(g) == 1 and g[0]["ctas"] == 1 and g[0]["points"] == 40
+
+
+def test_plan_rejects_inconsistent_layouts():
+    w = wl.cantilever(10, 0.1)
+    w.junction_valid[-1] = True          # a junction past the rod end
+    with pytest.raises(ValueError, match="junction_valid"):
+        plan(w)
+    big = World()
+    for _ in range(2):
+        big.add_rod(st.init_rod(12000, 24.0), st.RodParams())
+    big.finalize()
+    big.add_bindings(0, 1, BIND_BIDIRECTIONAL, stride=100)
+    with pytest.raises(NotImplementedError):
+        plan(big)
+
+
+@pytest.mark.skipif(have_gpu(), reason="checks the no-device failure path")
+def test_engine_fails_loudly_without_a_device():
+    from paper_2509_04277_b200.engine import Engine
+    with pytest.raises((ValueError, _lib.RodsimError)):
+        Engine(wl.cantilever())
+
+
+def test_engine_rejects_out_of_scope_scenes():
+    from paper_2509_04277_b200.engine import Engine
+    w = wl.cantilever()
+    w.set_mesh(object())
+    with pytest.raises(NotImplementedError, match="mesh"):
+        Engine(w)
+    with pytest.raises(ValueError):
+        Engine(wl.cantilever(), backend="gpu")

@@ -52,6 +52,35 @@ def parity(make, steps, k=None, **kw):
     return g
 
 
+# -- golden fixtures written by the reference package itself ------------------
+
+GOLDEN_BUILDERS = {
+    "cfg1_cantilever64": (wl.cantilever, 1000),
+    "cfg2_extensible512": (wl.extensible, 10),
+    "cfg3_pair2x512": (wl.pair, 10),
+    "cfg4_sweep256": (lambda: wl.sweep(256), 100),
+    "cfg4_sweep2048": (lambda: wl.sweep(2048), 10),
+    "cfg5_hair8": (lambda: wl.hair(8), 100),
+}
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN_BUILDERS))
+def test_gpu_matches_reference_golden_checkpoints(name):
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{name}.npz"))
+    make, k = GOLDEN_BUILDERS[name]
+    w = make()
+    done = 0
+    with Engine(w) as eng:
+        for c in g["checkpoints"]:
+            while done < c:
+                n = min(k, int(c) - done)
+                eng.run_epoch(n)
+                done += n
+            for key in STATE:
+                assert np.array_equal(getattr(w, key), g[f"step{c}_{key}"]), (c, key)
+
+
 # -- BASELINE configs (fp64 mirror: bitwise) ----------------------------------
 
 def test_cfg1_cantilever_1000_steps_bitwise():
