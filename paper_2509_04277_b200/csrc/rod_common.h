@@ -43,7 +43,8 @@ struct CtaTask {
     int32_t bind_seq;    // 1: bindings overlap (not a matching) -> ordered
     int32_t e_uni;       // element whose constants stand for the whole CTA
                          // when the launch uses CTA-uniform constants
-    int32_t pad[2];
+    int32_t e0;          // element of the first slot (single-rod tasks)
+    int32_t nrods;       // whole rods in the range (0: part of one rod)
 };
 
 // A binding endpoint pair resolved to (cta rank within the cluster, slot).
@@ -67,7 +68,9 @@ struct DrvEntry {
     int32_t pad;
 };
 
-enum Tier : int { TIER_CTA = 0, TIER_CLUSTER = 1, TIER_GRID = 2 };
+// TIER_STREAM: persistent CTAs, each stepping a sequence of single-rod tasks
+// and prefetching the next rod's state with TMA bulk copies (batches).
+enum Tier : int { TIER_CTA = 0, TIER_CLUSTER = 1, TIER_GRID = 2, TIER_STREAM = 3 };
 
 // Kernel arguments; device pointers, AoS layouts identical to world.py.
 template <typename Real>
@@ -96,6 +99,7 @@ struct StepArgs {
     int32_t debug;                                 // bit 0: poison smem (NaN) first
     int32_t any_binds;                             // launch has bindings (cluster/grid:
     int32_t any_grabs;                             //   barrier count must be uniform)
+    int32_t ntasks;                                // stream tier: tasks for gridDim CTAs
     Real dt, beta, gx, gy, gz;
 };
 

@@ -112,6 +112,10 @@ static cudaError_t dispatch(int what, int variant, int tier, bool uni, const Ste
             case 4: return RSB_D(3, 1152, TIER_CTA);
             case 5: return RSB_D(1, 160, TIER_CTA);
         }
+    } else if (tier == TIER_STREAM) {
+        switch (variant) {
+            case 5: return RSB_D(1, 160, TIER_STREAM);
+        }
     } else if (tier == TIER_CLUSTER) {
         switch (variant) {
             case 2: return RSB_D(2, 512, TIER_CLUSTER);

@@ -87,7 +87,8 @@ struct Group {       // one kernel launch
     int tier = TIER_CTA;
     int variant = 0;
     bool uni = false;
-    int task_begin = 0, ncta = 0;
+    int task_begin = 0, ncta = 0;   // tasks (one CTA each, except stream)
+    int grid = 0;                   // CTAs launched (stream: persistent)
     int threads = 0;
     int cluster = 1;
     int bind_cap = 0, drv_cap = 0;
@@ -161,7 +162,9 @@ int dev_alloc(DevBuf& b, size_t bytes) {
     b.p = nullptr;
     b.bytes = 0;
     if (bytes == 0) return RS_OK;
-    CK(cudaMalloc(&b.p, bytes));
+    // +64 B: the stream tier's 16-byte-aligned bulk copies may read up to
+    // 15 bytes past the last rod's block
+    CK(cudaMalloc(&b.p, bytes + 64));
     b.bytes = bytes;
     return RS_OK;
 }
@@ -364,7 +367,16 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         t.p0 = int32_t(p0);
         t.np = int32_t(np);
         t.e_uni = -1;
-        for (int64_t p = p0; p < p0 + np; ++p) task_of[p] = int32_t(h->h_tasks.size());
+        t.e0 = pt_elem[p0];
+        int nrods = 0;   // rods lying entirely inside the range
+        for (int64_t p = p0; p < p0 + np; ++p) {
+            task_of[p] = int32_t(h->h_tasks.size());
+            if (!(pflags[p] & SF_HAS_PREV) && p + 1 < p0 + np) {
+                const int64_t r = rod_of(d, p);
+                if (d.rod_offsets[r + 1] <= p0 + np) ++nrods;
+            }
+        }
+        t.nrods = nrods;
         h->h_tasks.push_back(t);
     };
 
@@ -554,9 +566,18 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         const int maxT = var.CAP / var.S;
         g.threads = std::min(maxT, ((max_np + var.S - 1) / var.S + 31) / 32 * 32);
         g.threads = std::max(g.threads, 32);
-        size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap).total
-                                        : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap).total;
-        const int stage_cap = SCRATCH_FIELDS * var.CAP / BIND_REALS;
+        // batches of whole single rods with no bindings: persistent stream
+        // tier (TMA prefetch of the next rod while the current one steps)
+        if (g.tier == TIER_CTA && g.variant == kBatchVariant && d.force_tier < 0) {
+            bool single = true;
+            for (int t = g.task_begin; t < g.task_begin + g.ncta && single; ++t)
+                single = h->h_tasks[t].nrods == 1 && h->h_tasks[t].bind_count == 0;
+            if (single) g.tier = TIER_STREAM;
+        }
+        const bool stream = g.tier == TIER_STREAM;
+        size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap, stream).total
+                                        : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap, stream).total;
+        const int stage_cap = BIND_FIELDS * var.CAP / BIND_REALS;
         if ((smem > kMaxSmem || g.bind_cap > stage_cap) && g.bind_cap > 0) {
             // no room to stage binding constants: apply bindings in order
             for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
@@ -572,6 +593,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         }
         if (smem > kMaxSmem) return fail(RS_E_UNSUPPORTED, "shared memory plan %zu B too large", smem);
         g.smem = smem;
+        g.grid = g.tier == TIER_STREAM ? std::min(g.ncta, min_blocks(var.S, var.CAP) * h->num_sms) : g.ncta;
         if (h->dry) continue;
         int occ = 0;
         int rc = occupancy_query(h, g.variant, g.tier, g.uni, g.threads, g.smem, g.cluster, &occ);
@@ -581,9 +603,10 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         if (g.tier == TIER_GRID && int64_t(occ) * h->num_sms < g.ncta)
             return fail(RS_E_UNSUPPORTED, "grid tier needs %d co-resident CTAs, device holds %d", g.ncta,
                         occ * h->num_sms);
-        if (g.tier == TIER_CTA && occ < 1)
+        if ((g.tier == TIER_CTA || g.tier == TIER_STREAM) && occ < 1)
             return fail(RS_E_UNSUPPORTED, "CTA plan cannot be resident (%zu B smem, %d threads)", g.smem,
                         g.threads);
+        if (g.tier == TIER_STREAM) g.grid = std::min(g.ncta, occ * h->num_sms);
         if (g.tier == TIER_GRID) {
             CK(cudaMalloc(&g.d_flags, sizeof(int32_t) * g.ncta));
             CK(cudaMalloc(&g.d_halo, h->rsz * 2 * HALO_WORDS * size_t(g.ncta)));
@@ -760,6 +783,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.drv_cap = g.drv_cap;
     a.has_fext = h->has_fext;
     a.ncta = g.ncta;
+    a.ntasks = g.ncta;
     a.debug = h->debug;
     for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
         a.any_binds |= h->h_tasks[t].bind_count > 0;
@@ -778,13 +802,13 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps) {
     cudaError_t e;
     if (h->prec == RS_F64_MIRROR) {
         auto a = make_args<double>(h, g, step0, steps);
-        e = mirror::launch_step<double>(g.variant, g.tier, g.uni, a, g.ncta, g.threads, g.smem, g.cluster, h->st);
+        e = mirror::launch_step<double>(g.variant, g.tier, g.uni, a, g.grid, g.threads, g.smem, g.cluster, h->st);
     } else if (h->prec == RS_F32) {
         auto a = make_args<float>(h, g, step0, steps);
-        e = fast::launch_step<float>(g.variant, g.tier, g.uni, a, g.ncta, g.threads, g.smem, g.cluster, h->st);
+        e = fast::launch_step<float>(g.variant, g.tier, g.uni, a, g.grid, g.threads, g.smem, g.cluster, h->st);
     } else {
         auto a = make_args<double>(h, g, step0, steps);
-        e = fast::launch_step<double>(g.variant, g.tier, g.uni, a, g.ncta, g.threads, g.smem, g.cluster, h->st);
+        e = fast::launch_step<double>(g.variant, g.tier, g.uni, a, g.grid, g.threads, g.smem, g.cluster, h->st);
     }
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
@@ -1049,14 +1073,14 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
         const Variant v = kVariants[g.variant];
         int64_t pts = 0;
         for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) pts += h->h_tasks[t].np;
+        static const char* names[] = {"cta", "cluster", "grid", "stream"};
         char tmp[512];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "
-                 "\"uniform\": %s, \"ctas\": %d, \"threads\": %d, \"cluster\": %d, \"smem\": %zu, "
-                 "\"points\": %lld, \"bind_cap\": %d}",
-                 i ? ", " : "", g.tier == TIER_CTA ? "cta" : (g.tier == TIER_CLUSTER ? "cluster" : "grid"),
-                 g.variant, v.S, v.CAP, g.uni ? "true" : "false", g.ncta, g.threads, g.cluster, g.smem,
-                 (long long)pts, g.bind_cap);
+                 "\"uniform\": %s, \"ctas\": %d, \"grid\": %d, \"threads\": %d, \"cluster\": %d, "
+                 "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d}",
+                 i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni ? "true" : "false", g.ncta,
+                 g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap);
         s += tmp;
     }
     s += "]}";

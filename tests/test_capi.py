@@ -83,8 +83,11 @@ def test_plan_pair_keeps_bound_rods_together_with_parallel_bindings():
 
 def test_plan_batched_rods_use_occupancy_variant():
     g = plan(wl.hair(2048))[0]
-    assert g["tier"] == "cta" and g["variant"] == 5 and g["ctas"] == 2048
-    assert g["threads"] == 160
+    # persistent stream tier: 2048 rod tasks over <= 4 CTAs per SM
+    assert g["tier"] == "stream" and g["variant"] == 5 and g["ctas"] == 2048
+    assert g["threads"] == 160 and g["grid"] <= 4 * 148
+    small = plan(wl.hair(16))[0]
+    assert small["tier"] == "cta"
 
 
 def test_plan_forced_tiers_and_variants():

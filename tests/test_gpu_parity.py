@@ -129,6 +129,25 @@ def test_cfg5_hair_sample_bitwise():
     parity(lambda: wl.hair(16), 200, 50)
 
 
+@pytest.mark.parametrize("k", [1, 7])
+def test_cfg5_stream_tier_bitwise(k):
+    # enough rods for the persistent TMA-prefetch stream tier
+    def make():
+        w = wl.hair(700)
+        for r in range(0, 700, 97):
+            w.set_driver(r)
+            w.driver_velocity[r] = (0.0, 0.01, 0.0)
+            w.driver_rotation[r] = 0.5
+        w.grab(3, 100, (0.05, 0.2, 0.1))
+        return w
+    g, r = make(), make()
+    plan = run_gpu(g, 14, k)
+    assert plan["groups"][0]["tier"] == "stream"
+    assert plan["groups"][0]["grid"] < plan["groups"][0]["ctas"]
+    OracleStepper(r).run(14)
+    assert_bitwise(g, r)
+
+
 # -- forced tiers on small rods (exercise DSMEM / halo paths cheaply) ---------
 
 @pytest.mark.parametrize("ctas", [2, 3, 5, 8, 16])
