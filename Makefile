@@ -7,7 +7,7 @@ NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v
 CSRC    := paper_2509_04277_b200/csrc
 LIB     := paper_2509_04277_b200/librodsim_b200.so
 HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/rodsim_b200.h
-OBJS    := build/rod_kernels_mirror.o build/rod_kernels_fast.o build/rodsim_capi.o
+OBJS    := build/rod_kernels_mirror.o build/rod_kernels_fast.o build/rodsim_capi.o build/rod_micro.o
 
 all: $(LIB) oracle/liboracle.so
 
@@ -20,6 +20,10 @@ build/rod_kernels_mirror.o: $(CSRC)/rod_kernels_mirror.cu $(HDRS) | build
 
 build/rod_kernels_fast.o: $(CSRC)/rod_kernels_fast.cu $(HDRS) | build
 	$(NVCC) $(NVFLAGS) --fmad=true -c $< -o $@ 2> build/ptxas_fast.log || (cat build/ptxas_fast.log; false)
+
+# latency microbenchmarks, mirror flags (the chains the mirror kernel issues)
+build/rod_micro.o: $(CSRC)/rod_micro.cu $(CSRC)/rod_math.cuh | build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC --fmad=false -prec-div=true -prec-sqrt=true -c $< -o $@
 
 build/rodsim_capi.o: $(CSRC)/rodsim_capi.cu $(HDRS) | build
 	$(NVCC) -std=c++17 $(ARCH) -O2 -Xcompiler -fPIC -c $< -o $@

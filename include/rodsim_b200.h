@@ -142,6 +142,13 @@ int rs_selftest_div(const double *a, const double *b, int64_t n, double *q_ieee,
 /* Measured issue rate of one pipe on the current device (operations/s):
  * kind 0 DFMA, 1 DADD, 2 DMUL, 3 FFMA.  Compute cross-check for the bench. */
 int rs_pipe_peak(int kind, double *ops_per_s);
+/* Latency microbenchmark for the single-rod latency roofline: kind 0 DADD,
+ * 1 DMUL, 2 DFMA, 3 IEEE div, 4 sqrt+add, 5 reciprocal-based div, 6 1/x
+ * (dependent chains), 7 shared-memory load chase, 8 bar.sync with `param`
+ * threads, 9 barrier.cluster across `param` CTAs (+ one DSMEM read per
+ * phase), 10 DSMEM load chase.  out[0] = cycles, out[1] = ns (0 if not
+ * measured) per operation / barrier. */
+int rs_micro(int kind, int param, double *out);
 
 #ifdef __cplusplus
 }

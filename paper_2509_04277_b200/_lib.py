@@ -86,7 +86,19 @@ SIGNATURES = [
     ("rs_timer_ms", _f64, [_p]),
     ("rs_pipe_peak", _i32, [_i32, ctypes.POINTER(_f64)]),
     ("rs_plan_dry", _i32, [ctypes.POINTER(WorldDesc), _i32, ctypes.c_char_p, _i64]),
+    ("rs_micro", _i32, [_i32, _i32, ctypes.POINTER(_f64)]),
 ]
+
+MICRO_KINDS = {"dadd": 0, "dmul": 1, "dfma": 2, "div": 3, "sqrt_add": 4, "div_rn": 5,
+               "rcp": 6, "lds": 7, "bar_sync": 8, "cluster_barrier": 9, "dsmem": 10}
+
+
+def micro(kind, param=0):
+    """(cycles, ns) per operation of a latency microbenchmark (rs_micro)."""
+    lib = load_library()
+    out = (_f64 * 2)()
+    check(lib.rs_micro(MICRO_KINDS.get(kind, kind), int(param), out), lib)
+    return out[0], out[1]
 
 
 def pipe_peak(kind):

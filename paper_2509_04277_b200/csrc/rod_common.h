@@ -96,12 +96,16 @@ struct StepArgs {
     int32_t drv_cap;                               // smem driver slots per CTA
     int32_t has_fext;
     int32_t ncta;
-    int32_t debug;                                 // bit 0: poison smem (NaN) first
+    int32_t debug;                                 // bit 0: poison smem (NaN) first,
+                                                   // bit 1: per-phase cycles -> prof
+    unsigned long long *prof;                      // (PROF_SLOTS) phase cycle sums
     int32_t any_binds;                             // launch has bindings (cluster/grid:
     int32_t any_grabs;                             //   barrier count must be uniform)
     int32_t ntasks;                                // stream tier: tasks for gridDim CTAs
     Real dt, beta, gx, gy, gz;
 };
+
+constexpr int PROF_SLOTS = 64;
 
 // grid-tier halo record per CTA and buffer (Real words)
 constexpr int HALO_WORDS = 32;

@@ -14,10 +14,12 @@
 namespace rsb {
 namespace RSB_MODE_NS {
 
-// (slots per thread S, slot capacity per CTA CAP); CAP/S threads is a
-// multiple of 128 so the register budget per thread is 65536/(CAP/S).
-//   V0 (1,128)  V1 (1,256)  V2 (2,512)  V3 (2,768)  V4 (3,1152)
-// Cluster and grid tiers use V2 or V4.
+// (slots per thread S, slot capacity per CTA CAP): up to max_threads(S, CAP)
+// threads cover S slots each (S odd: strided, S even: paired), CAP leaves
+// room for the tail slot.
+//   V0 (1,132)  V1 (1,258)  V2 (1,514)  V3 (2,770)  V4 (4,1154)
+//   V5 (1,130) and V6 (2,130): batches of 129-point rods, 5 CTAs per SM
+// Cluster tier: V0, V1, V2, V4; grid tier: V2, V4.
 
 template <typename Real, int S, int CAP, int TIER, bool UNI>
 static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
@@ -105,26 +107,30 @@ static cudaError_t dispatch(int what, int variant, int tier, bool uni, const Ste
 #define RSB_D(S, CAP, TIER) dispatch_uni<Real, S, CAP, TIER>(what, uni, a, ncta, threads, smem, cluster, st, out)
     if (tier == TIER_CTA) {
         switch (variant) {
-            case 0: return RSB_D(1, 128, TIER_CTA);
-            case 1: return RSB_D(1, 256, TIER_CTA);
-            case 2: return RSB_D(2, 512, TIER_CTA);
-            case 3: return RSB_D(2, 768, TIER_CTA);
-            case 4: return RSB_D(3, 1152, TIER_CTA);
-            case 5: return RSB_D(1, 160, TIER_CTA);
+            case 0: return RSB_D(1, 132, TIER_CTA);
+            case 1: return RSB_D(1, 258, TIER_CTA);
+            case 2: return RSB_D(1, 514, TIER_CTA);
+            case 3: return RSB_D(2, 770, TIER_CTA);
+            case 4: return RSB_D(4, 1154, TIER_CTA);
+            case 5: return RSB_D(1, 130, TIER_CTA);
+            case 6: return RSB_D(2, 130, TIER_CTA);
         }
     } else if (tier == TIER_STREAM) {
         switch (variant) {
-            case 5: return RSB_D(1, 160, TIER_STREAM);
+            case 5: return RSB_D(1, 130, TIER_STREAM);
+            case 6: return RSB_D(2, 130, TIER_STREAM);
         }
     } else if (tier == TIER_CLUSTER) {
         switch (variant) {
-            case 2: return RSB_D(2, 512, TIER_CLUSTER);
-            case 4: return RSB_D(3, 1152, TIER_CLUSTER);
+            case 0: return RSB_D(1, 132, TIER_CLUSTER);
+            case 1: return RSB_D(1, 258, TIER_CLUSTER);
+            case 2: return RSB_D(1, 514, TIER_CLUSTER);
+            case 4: return RSB_D(4, 1154, TIER_CLUSTER);
         }
     } else if (tier == TIER_GRID) {
         switch (variant) {
-            case 2: return RSB_D(2, 512, TIER_GRID);
-            case 4: return RSB_D(3, 1152, TIER_GRID);
+            case 2: return RSB_D(1, 514, TIER_GRID);
+            case 4: return RSB_D(4, 1154, TIER_GRID);
         }
     }
 #undef RSB_D

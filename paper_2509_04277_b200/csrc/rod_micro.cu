@@ -1,0 +1,196 @@
+// rod_micro.cu -- latency microbenchmarks behind the single-rod latency
+// roofline t_floor = n_sync * (t_sync + t_chain) + t_launch / K:
+// dependent fp64 chains (the per-phase critical path is built from these),
+// shared-memory load latency, and the three barrier scopes the step kernel
+// uses (bar.sync in a CTA, barrier.cluster across a cluster, DSMEM reads).
+// Compiled with the mirror flags (--fmad=false, IEEE div/sqrt) so the chains
+// are the instruction sequences the fp64 mirror kernel issues.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rod_math.cuh"
+
+namespace rsb {
+namespace micro {
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// out[0] = cycles per op, out[1] = ns per op (thread 0, dependent chain)
+template <int KIND>
+__global__ void chain_kernel(double* out, int iters, double a, double b) {
+    if (threadIdx.x != 0) return;
+    double x = a, rb = 1.0 / b;
+    const long long c0 = clock64();
+    const uint64_t t0 = gtimer();
+    for (int i = 0; i < iters; ++i) {
+        if constexpr (KIND == 0) x = x + b;
+        else if constexpr (KIND == 1) x = x * b;
+        else if constexpr (KIND == 2) x = fma(x, b, a);
+        else if constexpr (KIND == 3) x = x / b;
+        else if constexpr (KIND == 4) x = sqrt(x) + a;
+        else if constexpr (KIND == 5) x = div_rn(x, b, rb);
+        else if constexpr (KIND == 6) x = 1.0 / x;
+    }
+    const long long c1 = clock64();
+    const uint64_t t1 = gtimer();
+    out[0] = double(c1 - c0) / iters;
+    out[1] = double(t1 - t0) / iters;
+    if (x == 12345.678) out[2] = x;
+}
+
+// shared-memory pointer chase: cycles per dependent LDS
+__global__ void lds_kernel(double* out, int iters) {
+    __shared__ int nxt[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) nxt[i] = (i + 97) & 1023;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    int p = 0;
+    const long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) p = nxt[p];
+    const long long c1 = clock64();
+    out[0] = double(c1 - c0) / iters;
+    out[1] = 0;
+    if (p == -1) out[2] = p;
+}
+
+// CTA barrier: ns per bar.sync with blockDim threads, each with a little
+// shared-memory traffic per phase like the step kernel's
+__global__ void bar_kernel(double* out, int iters) {
+    __shared__ double buf[1024];
+    const int t = threadIdx.x;
+    buf[t] = t;
+    __syncthreads();
+    const uint64_t t0 = gtimer();
+    const long long c0 = clock64();
+    double acc = 0;
+    for (int i = 0; i < iters; ++i) {
+        acc += buf[(t + i) & (blockDim.x - 1)];
+        __syncthreads();
+        buf[t] = acc;
+        __syncthreads();
+    }
+    const long long c1 = clock64();
+    const uint64_t t1 = gtimer();
+    if (t == 0) {
+        out[0] = double(c1 - c0) / (2.0 * iters);
+        out[1] = double(t1 - t0) / (2.0 * iters);
+    }
+    if (acc == -1.0) out[2] = acc;
+}
+
+// cluster barrier (arrive.release + wait.acquire) with one DSMEM read of the
+// neighbour's slot per phase: ns per phase
+__global__ void cluster_bar_kernel(double* out, int iters) {
+    __shared__ double buf[32];
+    unsigned rank, nrank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nrank));
+    if (threadIdx.x < 32) buf[threadIdx.x] = rank;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(buf)), remote;
+    const unsigned nb = (rank + 1) % nrank;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(nb));
+    double acc = 0;
+    const uint64_t t0 = gtimer();
+    const long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        double v;
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+        acc += v;
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    const long long c1 = clock64();
+    const uint64_t t1 = gtimer();
+    if (rank == 0 && threadIdx.x == 0) {
+        out[0] = double(c1 - c0) / iters;
+        out[1] = double(t1 - t0) / iters;
+    }
+    if (acc == -1.0) out[2] = acc;
+}
+
+// DSMEM dependent remote load latency (thread 0 of rank 0 chases through
+// rank 1's shared memory)
+__global__ void dsmem_kernel(double* out, int iters) {
+    __shared__ int nxt[256];
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) nxt[i] = (i + 31) & 255;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (rank == 0 && threadIdx.x == 0) {
+        uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(nxt)), rbase;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbase) : "r"(base), "r"(1));
+        int p = 0;
+        const long long c0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            int v;
+            asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(rbase + 4u * p) : "memory");
+            p = v;
+        }
+        const long long c1 = clock64();
+        out[0] = double(c1 - c0) / iters;
+        out[1] = 0;
+        if (p == -1) out[2] = p;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// kind: 0 DADD, 1 DMUL, 2 DFMA, 3 IEEE div, 4 sqrt(+add), 5 div_rn, 6 1/x
+//       (chains; param unused), 7 LDS chase, 8 bar.sync (param = threads),
+//       9 cluster barrier (param = CTAs), 10 DSMEM chase (2-CTA cluster)
+cudaError_t run(int kind, int param, double* res) {
+    double* buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, 4 * sizeof(double));
+    if (e != cudaSuccess) return e;
+    const int iters = 4096;
+    auto launch = [&]() -> cudaError_t {
+        switch (kind) {
+            case 0: chain_kernel<0><<<1, 32>>>(buf, iters, 1.0, 1e-9); break;
+            case 1: chain_kernel<1><<<1, 32>>>(buf, iters, 1.0, 1.0000001); break;
+            case 2: chain_kernel<2><<<1, 32>>>(buf, iters, 1e-9, 0.999); break;
+            case 3: chain_kernel<3><<<1, 32>>>(buf, iters, 1.0, 1.0000001); break;
+            case 4: chain_kernel<4><<<1, 32>>>(buf, iters, 0.5, 1.0); break;
+            case 5: chain_kernel<5><<<1, 32>>>(buf, iters, 1.0, 1.0000001); break;
+            case 6: chain_kernel<6><<<1, 32>>>(buf, iters, 1.5, 1.0); break;
+            case 7: lds_kernel<<<1, 32>>>(buf, iters); break;
+            case 8: bar_kernel<<<1, param>>>(buf, iters); break;
+            case 9:
+            case 10: {
+                cudaLaunchConfig_t cfg = {};
+                const int c = kind == 9 ? param : 2;
+                cfg.gridDim = dim3(c);
+                cfg.blockDim = dim3(kind == 9 ? 128 : 32);
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = c;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                if (kind == 9) {
+                    if (c > 8) cudaFuncSetAttribute(cluster_bar_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                    return cudaLaunchKernelEx(&cfg, cluster_bar_kernel, buf, iters);
+                }
+                return cudaLaunchKernelEx(&cfg, dsmem_kernel, buf, iters);
+            }
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    };
+    e = launch();   // warm-up
+    if (e == cudaSuccess) e = launch();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(res, buf, 2 * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    return e;
+}
+
+}  // namespace micro
+}  // namespace rsb
+
+extern "C" int rs_micro(int kind, int param, double* cycles_ns) {
+    return rsb::micro::run(kind, param, cycles_ns) == cudaSuccess ? 0 : -2;
+}

@@ -66,10 +66,13 @@ int fail(int code, const char* fmt, ...) {
 
 struct Variant {
     int S, CAP;
+    // slots the threads cover; one more (the element-less tail) fits in CAP
+    constexpr int cover() const { return S * max_threads(S, CAP); }
 };
-// capacity-ordered variants 0..4, then the occupancy-tuned batched variant 5
-constexpr Variant kVariants[] = {{1, 128}, {1, 256}, {2, 512}, {2, 768}, {3, 1152}, {1, 160}};
-constexpr int kNumVariants = 6;
+// capacity-ordered variants 0..4, then the batched variants 5 (strided, 128
+// threads) and 6 (paired, 64 threads) for 129-point rods
+constexpr Variant kVariants[] = {{1, 132}, {1, 258}, {1, 514}, {2, 770}, {4, 1154}, {1, 130}, {2, 130}};
+constexpr int kNumVariants = 7;
 constexpr int kNumCapVariants = 5;
 constexpr int kBatchVariant = 5;
 constexpr int kClusterVariant = 4;
@@ -125,6 +128,8 @@ struct rs_handle_s {
     DevBuf pflags, pt_elem, tasks, binds, drvs, grabs;
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;   // pinned
+    unsigned long long* d_prof = nullptr;  // RSB_DEBUG bit 1: per-phase cycles (CTA 0)
+    int64_t prof_steps = 0;
     int has_fext = 0;
 
     // plan
@@ -333,7 +338,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     }
 
     // -- choose tiers --------------------------------------------------------
-    const int cta_cap = kVariants[kNumCapVariants - 1].CAP;
+    const int cta_cap = kVariants[kNumCapVariants - 1].cover();
     std::vector<int> seg_tier(segs.size());
     int64_t max_cta_seg = 0;
     for (size_t i = 0; i < segs.size(); ++i) {
@@ -383,16 +388,16 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     // CTA tier: pack consecutive CTA-tier segments into CTAs
     if (max_cta_seg > 0) {
         int v = 0;
-        while (kVariants[v].CAP < max_cta_seg) ++v;
-        // batches of short rods: one rod per 160-thread CTA, 4 CTAs per SM
+        while (kVariants[v].cover() + 1 < max_cta_seg) ++v;
+        // batches of short rods: one rod per 64-thread CTA, 5 CTAs per SM
         int64_t cta_points = 0;
         for (size_t i = 0; i < segs.size(); ++i)
             if (seg_tier[i] == TIER_CTA) cta_points += segs[i].p1 - segs[i].p0;
-        if (max_cta_seg <= kVariants[kBatchVariant].CAP &&
+        if (max_cta_seg <= kVariants[kBatchVariant].cover() + 1 &&
             cta_points >= int64_t(2) * kVariants[kBatchVariant].CAP * h->num_sms)
             v = kBatchVariant;
         if (d.force_variant >= 0) {
-            if (d.force_variant >= kNumVariants || kVariants[d.force_variant].CAP < max_cta_seg)
+            if (d.force_variant >= kNumVariants || kVariants[d.force_variant].cover() + 1 < max_cta_seg)
                 return fail(RS_E_INVALID, "force_variant %d cannot hold %lld points", d.force_variant,
                             (long long)max_cta_seg);
             v = d.force_variant;
@@ -401,7 +406,8 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         g.tier = TIER_CTA;
         g.variant = v;
         g.task_begin = int(h->h_tasks.size());
-        const int cap = kVariants[v].CAP;
+        // packed tasks end at a rod end, so the tail slot is usable
+        const int cap = std::min(kVariants[v].CAP, kVariants[v].cover() + 1);
         int64_t cur0 = -1, cur1 = -1;
         for (size_t i = 0; i < segs.size(); ++i) {
             if (seg_tier[i] != TIER_CTA) {
@@ -429,8 +435,10 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         Group g;
         g.tier = seg_tier[i];
         g.variant = kClusterVariant;
-        if (d.force_variant == 2 || d.force_variant == 4) g.variant = d.force_variant;
-        const int cap = kVariants[g.variant].CAP;
+        if (d.force_variant >= 0 && d.force_variant <= 4 && d.force_variant != 3 &&
+            (g.tier == TIER_CLUSTER || d.force_variant == 2 || d.force_variant == 4))
+            g.variant = d.force_variant;
+        const int cap = kVariants[g.variant].cover();
         int c = int((np + cap - 1) / cap);
         if (d.force_ctas > 0) c = std::max(c, int(d.force_ctas));
         c = int(std::min<int64_t>(c, np));
@@ -563,12 +571,23 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         g.uni = uni;
         g.bind_cap = bcap;
         g.drv_cap = std::max(dcap, 1);
-        const int maxT = var.CAP / var.S;
-        g.threads = std::min(maxT, ((max_np + var.S - 1) / var.S + 31) / 32 * 32);
-        g.threads = std::max(g.threads, 32);
+        // slots the threads must cover: a task whose last slot is a rod end
+        // (no element) leaves it to thread 0 as the tail slot
+        int need = 0;
+        for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
+            const CtaTask& tk = h->h_tasks[t];
+            const bool tail_ok = !(pflags[tk.p0 + tk.np - 1] & SF_HAS_ELEM);
+            need = std::max(need, tk.np - (tail_ok ? 1 : 0));
+        }
+        const int maxT = max_threads(var.S, var.CAP);
+        g.threads = std::max(32, ((need + var.S - 1) / var.S + 31) / 32 * 32);
+        if (g.threads > maxT || max_np > var.CAP || max_np > var.S * g.threads + 1)
+            return fail(RS_E_INVALID, "variant %d (S=%d, CAP=%d) cannot hold a %d-point task", g.variant, var.S,
+                        var.CAP, max_np);
         // batches of whole single rods with no bindings: persistent stream
         // tier (TMA prefetch of the next rod while the current one steps)
-        if (g.tier == TIER_CTA && g.variant == kBatchVariant && d.force_tier < 0) {
+        if (g.tier == TIER_CTA && (g.variant == kBatchVariant || g.variant == kBatchVariant + 1) &&
+            d.force_tier < 0) {
             bool single = true;
             for (int t = g.task_begin; t < g.task_begin + g.ncta && single; ++t)
                 single = h->h_tasks[t].nrods == 1 && h->h_tasks[t].bind_count == 0;
@@ -785,6 +804,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.ncta = g.ncta;
     a.ntasks = g.ncta;
     a.debug = h->debug;
+    a.prof = h->d_prof;
     for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
         a.any_binds |= h->h_tasks[t].bind_count > 0;
         a.any_grabs |= h->h_tasks[t].grab_count > 0;
@@ -868,6 +888,9 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     *h->h_err = 0;
     if (cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess)
         return bail(fail(RS_E_CUDA, "memset failed"));
+    if ((h->debug & 2) && (cudaMalloc(&h->d_prof, PROF_SLOTS * sizeof(unsigned long long)) != cudaSuccess ||
+                           cudaMemset(h->d_prof, 0, PROF_SLOTS * sizeof(unsigned long long)) != cudaSuccess))
+        return bail(fail(RS_E_CUDA, "profile buffer allocation failed"));
     if (h->rsz == sizeof(double)) {
         register_host(h, h->d.pos, 3 * sizeof(double) * size_t(h->d.P));
         register_host(h, h->d.vel, 3 * sizeof(double) * size_t(h->d.P));
@@ -921,6 +944,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
         }
         done += k;
     }
+    h->prof_steps += steps;
     if (h->timing) CK(cudaEventRecord(h->ev1, h->st));
     h->timed = h->timing;
     CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
@@ -1020,6 +1044,19 @@ void rs_destroy(rs_handle h) {
         if (g.d_halo) cudaFree(g.d_halo);
     }
     for (void* p : h->registered) cudaHostUnregister(p);
+    if (h->d_prof) {   // per-phase profile (RSB_DEBUG=2): cycles per step, CTA 0
+        unsigned long long v[PROF_SLOTS];
+        if (cudaMemcpy(v, h->d_prof, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess && h->prof_steps > 0) {
+            fprintf(stderr, "rsb-prof steps=%lld cycles/step per phase:", (long long)h->prof_steps);
+            double tot = 0;
+            for (int i = 0; i < PROF_SLOTS && v[i]; ++i) {
+                fprintf(stderr, " %.0f", double(v[i]) / double(h->prof_steps));
+                tot += double(v[i]) / double(h->prof_steps);
+            }
+            fprintf(stderr, " | total %.0f\n", tot);
+        }
+        cudaFree(h->d_prof);
+    }
     if (h->d_err) cudaFree(h->d_err);
     if (h->h_err) cudaFreeHost(h->h_err);
     if (h->stage) cudaFreeHost(h->stage);

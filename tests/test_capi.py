@@ -83,9 +83,12 @@ def test_plan_pair_keeps_bound_rods_together_with_parallel_bindings():
 
 def test_plan_batched_rods_use_occupancy_variant():
     g = plan(wl.hair(2048))[0]
-    # persistent stream tier: 2048 rod tasks over <= 4 CTAs per SM
+    # persistent stream tier: 2048 rod tasks over <= 5 CTAs per SM; a
+    # 129-point rod is 128 threads plus the tip as thread 0's tail slot
     assert g["tier"] == "stream" and g["variant"] == 5 and g["ctas"] == 2048
-    assert g["threads"] == 160 and g["grid"] <= 4 * 148
+    assert g["threads"] == 128 and g["grid"] <= 5 * 148
+    paired = plan(wl.hair(2048), force_variant=6)[0]
+    assert paired["tier"] == "stream" and paired["threads"] == 64
     small = plan(wl.hair(16))[0]
     assert small["tier"] == "cta"
 

@@ -29,7 +29,9 @@ def _diff(a, b):
 
 
 def assert_bitwise(gpu_world, ref_world):
-    same = {k: np.array_equal(getattr(gpu_world, k), getattr(ref_world, k)) for k in STATE}
+    # raw bits: also distinguishes -0.0 from +0.0, which np.array_equal does not
+    same = {k: np.array_equal(getattr(gpu_world, k).view(np.int64), getattr(ref_world, k).view(np.int64))
+            for k in STATE}
     assert all(same.values()), f"not bitwise: {same} max|d| {_diff(gpu_world, ref_world)}"
 
 
@@ -129,19 +131,19 @@ def test_cfg5_hair_sample_bitwise():
     parity(lambda: wl.hair(16), 200, 50)
 
 
-@pytest.mark.parametrize("k", [1, 7])
-def test_cfg5_stream_tier_bitwise(k):
+@pytest.mark.parametrize("k,variant", [(1, 5), (7, 5), (1, 6), (7, 6)])
+def test_cfg5_stream_tier_bitwise(k, variant):
     # enough rods for the persistent TMA-prefetch stream tier
     def make():
-        w = wl.hair(700)
-        for r in range(0, 700, 97):
+        w = wl.hair(1700)
+        for r in range(0, 1700, 97):
             w.set_driver(r)
             w.driver_velocity[r] = (0.0, 0.01, 0.0)
             w.driver_rotation[r] = 0.5
         w.grab(3, 100, (0.05, 0.2, 0.1))
         return w
     g, r = make(), make()
-    plan = run_gpu(g, 14, k)
+    plan = run_gpu(g, 14, k, force_variant=variant)
     assert plan["groups"][0]["tier"] == "stream"
     assert plan["groups"][0]["grid"] < plan["groups"][0]["ctas"]
     OracleStepper(r).run(14)
@@ -181,7 +183,7 @@ def test_cluster_pair_overlapping_bindings_sequential_bitwise():
     parity(make, 60, 20, force_tier=1, force_ctas=3)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 def test_cta_variants_bitwise(variant):
     parity(lambda: wl.cantilever(100, 0.2), 100, 50, force_variant=variant)
 
