@@ -102,6 +102,14 @@ int rs_upload(rs_handle h, uint32_t mask);
  * 0 (barriers are on-chip).  Either pointer may be NULL. */
 int rs_run_epoch(rs_handle h, int64_t steps, int64_t *contacts, int64_t *barrier_ns);
 int rs_download(rs_handle h, uint32_t mask);
+/* rs_upload(RS_STATE) + rs_run_epoch + rs_download(RS_STATE) as one call
+ * (the host arrays are authoritative before and after, like the reference's
+ * in-place step_serial x K, _core.pyx:1058-1080).  For a plan of
+ * independent rods (one CTA/stream-tier launch, fp64) the epoch runs in
+ * chunks of rods on three streams so the H2D copy of chunk c+1 and the D2H
+ * copy of chunk c-1 overlap the launch on chunk c; results are identical
+ * to the sequential sequence.  Synchronous. */
+int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t *contacts, int64_t *barrier_ns);
 int rs_synchronize(rs_handle h);
 int64_t rs_error_step(rs_handle h);
 int64_t rs_step_counter(rs_handle h);

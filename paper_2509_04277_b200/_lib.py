@@ -66,6 +66,7 @@ SIGNATURES = [
     ("rs_upload", _i32, [_p, ctypes.c_uint32]),
     ("rs_run_epoch", _i32, [_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     ("rs_download", _i32, [_p, ctypes.c_uint32]),
+    ("rs_run_epoch_host", _i32, [_p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     ("rs_synchronize", _i32, [_p]),
     ("rs_error_step", _i64, [_p]),
     ("rs_step_counter", _i64, [_p]),
@@ -245,6 +246,14 @@ class DeviceWorld:
         contacts, bns = _i64(0), _i64(0)
         check(self.lib.rs_run_epoch(self.handle, int(steps), ctypes.byref(contacts),
                                     ctypes.byref(bns)), self.lib)
+        return contacts.value, bns.value
+
+    def run_host(self, steps):
+        """Upload the state, run `steps` steps, download the state (one
+        call, copies pipelined with the launches where the plan allows)."""
+        contacts, bns = _i64(0), _i64(0)
+        check(self.lib.rs_run_epoch_host(self.handle, int(steps), ctypes.byref(contacts),
+                                         ctypes.byref(bns)), self.lib)
         return contacts.value, bns.value
 
     def download(self, mask=RS_STATE):

@@ -112,12 +112,15 @@ struct rs_handle_s {
     int prec = RS_F64_MIRROR;
     size_t rsz = 8;                 // sizeof(Real) on the device
     cudaStream_t st = nullptr;
+    cudaStream_t st_in = nullptr, st_out = nullptr;   // pipelined host epochs: H2D, D2H
+    std::vector<cudaEvent_t> ev_in, ev_k;             // per-chunk copy / kernel events
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // per-epoch kernel timing
     cudaEvent_t tm0 = nullptr, tm1 = nullptr;   // caller-bracketed spans
     bool timing = false;
     bool timed = false;
     double last_ms = 0.0;
     int64_t launches = 0;
+    int64_t launches_pipelined = 0;   // epochs run by run_epoch_pipelined
     int num_sms = 0;
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
@@ -151,6 +154,11 @@ struct rs_handle_s {
     int64_t ring_apply[kRingCap];
     int64_t head = 0, tail = 0;
     bool control_dirty = false;
+    // last uploaded controls (upload_control skips unchanged ones)
+    bool ctl_valid = false;
+    std::vector<double> ctl_drv_v, ctl_drv_rot, ctl_g_tgt;
+    std::vector<uint8_t> ctl_g_act;
+    std::vector<int64_t> ctl_g_pt;
     int64_t snap_seq = 0, snap_step = 0;
 
     // host staging (pinned) for precision conversion
@@ -721,8 +729,24 @@ int upload_static(rs_handle h) {
     return build_grabs(h);
 }
 
+// Driver velocities/rotations and grab slots, re-sent only when they differ
+// from the last upload (they are read every epoch, like the reference's live
+// reads of the World arrays, but rarely change between epochs).
 int upload_control(rs_handle h) {
     const rs_world_desc& d = h->d;
+    const size_t R = size_t(d.R), G = size_t(d.ngrab);
+    auto same = [](const auto& v, const auto* p, size_t n) {
+        return v.size() == n && (n == 0 || std::memcmp(v.data(), p, n * sizeof(*p)) == 0);
+    };
+    if (h->ctl_valid && h->planned && same(h->ctl_drv_v, d.drv_v, 3 * R) && same(h->ctl_drv_rot, d.drv_rot, R) &&
+        same(h->ctl_g_act, d.g_act, G) && same(h->ctl_g_pt, d.g_pt, G) && same(h->ctl_g_tgt, d.g_tgt, 3 * G))
+        return RS_OK;
+    h->ctl_drv_v.assign(d.drv_v, d.drv_v + 3 * R);
+    h->ctl_drv_rot.assign(d.drv_rot, d.drv_rot + R);
+    h->ctl_g_act.assign(d.g_act, d.g_act + G);
+    h->ctl_g_pt.assign(d.g_pt, d.g_pt + G);
+    h->ctl_g_tgt.assign(d.g_tgt, d.g_tgt + 3 * G);
+    h->ctl_valid = h->planned;
     int rc = put_real(h, h->drv_v, d.drv_v, 3 * size_t(d.R));
     if (rc) return rc;
     if ((rc = put_real(h, h->drv_rot, d.drv_rot, size_t(d.R)))) return rc;
@@ -817,18 +841,30 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     return a;
 }
 
-int launch_group(rs_handle h, const Group& g, int64_t step0, int steps) {
+// Launch one group, or (t_cnt >= 0, CTA/stream tiers only) the task
+// sub-range [t_off, t_off + t_cnt) of it: tasks of those tiers are
+// independent, so a sub-range is a complete launch of its own.
+int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_off = 0, int t_cnt = -1) {
     if (g.tier == TIER_GRID) CK(cudaMemsetAsync(g.d_flags, 0, sizeof(int32_t) * g.ncta, h->st));
+    const int nt = t_cnt < 0 ? g.ncta : t_cnt;
+    const int grid = t_cnt < 0 ? g.grid : (g.tier == TIER_STREAM ? std::min(g.grid, nt) : nt);
+    auto sub = [&](auto& a) {
+        a.tasks += t_off;
+        a.ntasks = nt;
+    };
     cudaError_t e;
     if (h->prec == RS_F64_MIRROR) {
         auto a = make_args<double>(h, g, step0, steps);
-        e = mirror::launch_step<double>(g.variant, g.tier, g.uni, a, g.grid, g.threads, g.smem, g.cluster, h->st);
+        sub(a);
+        e = mirror::launch_step<double>(g.variant, g.tier, g.uni, a, grid, g.threads, g.smem, g.cluster, h->st);
     } else if (h->prec == RS_F32) {
         auto a = make_args<float>(h, g, step0, steps);
-        e = fast::launch_step<float>(g.variant, g.tier, g.uni, a, g.grid, g.threads, g.smem, g.cluster, h->st);
+        sub(a);
+        e = fast::launch_step<float>(g.variant, g.tier, g.uni, a, grid, g.threads, g.smem, g.cluster, h->st);
     } else {
         auto a = make_args<double>(h, g, step0, steps);
-        e = fast::launch_step<double>(g.variant, g.tier, g.uni, a, g.grid, g.threads, g.smem, g.cluster, h->st);
+        sub(a);
+        e = fast::launch_step<double>(g.variant, g.tier, g.uni, a, grid, g.threads, g.smem, g.cluster, h->st);
     }
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
@@ -846,6 +882,92 @@ void register_host(rs_handle h, void* p, size_t bytes) {
 }
 
 }  // namespace
+
+// ph_boundary at the epoch's first step: staged commands, dirty controls
+int epoch_prelude(rs_handle h) {
+    drain_ring(h);
+    if (h->control_dirty) {
+        int rc = upload_control(h);
+        if (rc) return rc;
+        h->control_dirty = false;
+    }
+    return RS_OK;
+}
+
+// after the epoch's launches (on h->st): error stamp read-back, counters
+int epoch_epilogue(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
+    if (h->timing) CK(cudaEventRecord(h->ev1, h->st));
+    h->timed = h->timing;
+    CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+    h->step += steps;
+    h->snap_seq += 2 * steps;
+    h->snap_step = h->step;
+    if (contacts) *contacts = 0;
+    if (barrier_ns) *barrier_ns = 0;
+    return RS_OK;
+}
+
+constexpr int kPipeChunks = 16;
+
+// One epoch with the state coming from and going back to the host arrays,
+// the copies of chunk c+1 (H2D) and c-1 (D2H) overlapping the launch on
+// chunk c.  Chunks are contiguous task ranges of a single CTA/stream-tier
+// group (whole rods, no cross-task coupling), so each chunk's launch is a
+// complete step of its rods and the result is identical to the unchunked
+// epoch.
+int run_epoch_pipelined(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
+    const Group& g = h->groups[0];
+    const rs_world_desc& d = h->d;
+    const int C = std::min(g.ncta, kPipeChunks);
+    if (!h->st_in) {
+        CK(cudaStreamCreateWithFlags(&h->st_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->st_out, cudaStreamNonBlocking));
+    }
+    while (int(h->ev_in.size()) < C + 1) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        h->ev_in.push_back(a);
+        h->ev_k.push_back(b);
+    }
+    // everything already queued on the compute stream (control uploads,
+    // earlier epochs) precedes this epoch's copies
+    CK(cudaEventRecord(h->ev_k[C], h->st));
+    CK(cudaStreamWaitEvent(h->st_in, h->ev_k[C], 0));
+    if (h->timing) CK(cudaEventRecord(h->ev0, h->st));
+    double* const hp[4] = {d.pos, d.vel, d.q, d.w};
+    DevBuf* const dp[4] = {&h->pos, &h->vel, &h->q, &h->w};
+    const int width[4] = {3, 3, 4, 3};
+    for (int c = 0; c < C; ++c) {
+        const int t0 = int(int64_t(g.ncta) * c / C), t1 = int(int64_t(g.ncta) * (c + 1) / C);
+        const CtaTask& a = h->h_tasks[g.task_begin + t0];
+        const CtaTask& b = h->h_tasks[g.task_begin + t1 - 1];
+        const int64_t P0 = a.p0, P1 = int64_t(b.p0) + b.np;
+        const int64_t E0 = P0 - rod_of(d, P0), E1 = P1 - (rod_of(d, P1 - 1) + 1);
+        for (int f = 0; f < 4; ++f) {
+            const int64_t r0 = f < 2 ? P0 : E0, r1 = f < 2 ? P1 : E1;
+            const size_t off = size_t(r0) * width[f], cnt = size_t(r1 - r0) * width[f];
+            CK(cudaMemcpyAsync(static_cast<double*>(dp[f]->p) + off, hp[f] + off, cnt * sizeof(double),
+                               cudaMemcpyHostToDevice, h->st_in));
+        }
+        CK(cudaEventRecord(h->ev_in[c], h->st_in));
+        CK(cudaStreamWaitEvent(h->st, h->ev_in[c], 0));
+        int rc = launch_group(h, g, h->step, int(steps), t0, t1 - t0);
+        if (rc) return rc;
+        CK(cudaEventRecord(h->ev_k[c], h->st));
+        CK(cudaStreamWaitEvent(h->st_out, h->ev_k[c], 0));
+        for (int f = 0; f < 4; ++f) {
+            const int64_t r0 = f < 2 ? P0 : E0, r1 = f < 2 ? P1 : E1;
+            const size_t off = size_t(r0) * width[f], cnt = size_t(r1 - r0) * width[f];
+            CK(cudaMemcpyAsync(hp[f] + off, static_cast<const double*>(dp[f]->p) + off, cnt * sizeof(double),
+                               cudaMemcpyDeviceToHost, h->st_out));
+        }
+    }
+    int rc = epoch_epilogue(h, steps, contacts, barrier_ns);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(h->st_out));
+    return rs_synchronize(h);
+}
 
 // ---- C ABI --------------------------------------------------------------------
 
@@ -928,12 +1050,8 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
     if (!h) return fail(RS_E_INVALID, "null handle");
     if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
     CK(cudaSetDevice(h->d.device));
-    drain_ring(h);
-    if (h->control_dirty) {
-        int rc = upload_control(h);
-        if (rc) return rc;
-        h->control_dirty = false;
-    }
+    int rc = epoch_prelude(h);
+    if (rc) return rc;
     if (h->timing) CK(cudaEventRecord(h->ev0, h->st));
     int64_t done = 0;
     while (done < steps) {
@@ -945,15 +1063,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
         done += k;
     }
     h->prof_steps += steps;
-    if (h->timing) CK(cudaEventRecord(h->ev1, h->st));
-    h->timed = h->timing;
-    CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
-    h->step += steps;
-    h->snap_seq += 2 * steps;
-    h->snap_step = h->step;
-    if (contacts) *contacts = 0;
-    if (barrier_ns) *barrier_ns = 0;
-    return RS_OK;
+    return epoch_epilogue(h, steps, contacts, barrier_ns);
 }
 
 int rs_synchronize(rs_handle h) {
@@ -982,6 +1092,25 @@ int rs_download(rs_handle h, uint32_t mask) {
         if ((rc = get_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
     }
     return rs_synchronize(h);
+}
+
+int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
+    CK(cudaSetDevice(h->d.device));
+    const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 &&
+                           (h->groups[0].tier == TIER_CTA || h->groups[0].tier == TIER_STREAM) &&
+                           h->groups[0].ncta >= 2 && steps <= kMaxStepsPerLaunch;
+    if (!pipelined) {
+        int rc = upload_state(h);
+        if (rc) return rc;
+        if ((rc = rs_run_epoch(h, steps, contacts, barrier_ns))) return rc;
+        return rs_download(h, RS_STATE);
+    }
+    int rc = epoch_prelude(h);
+    if (rc) return rc;
+    h->launches_pipelined += 1;
+    return run_epoch_pipelined(h, steps, contacts, barrier_ns);
 }
 
 int64_t rs_error_step(rs_handle h) {
@@ -1064,6 +1193,10 @@ void rs_destroy(rs_handle h) {
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->tm0) cudaEventDestroy(h->tm0);
     if (h->tm1) cudaEventDestroy(h->tm1);
+    for (cudaEvent_t e : h->ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_k) cudaEventDestroy(e);
+    if (h->st_in) cudaStreamDestroy(h->st_in);
+    if (h->st_out) cudaStreamDestroy(h->st_out);
     if (h->st) cudaStreamDestroy(h->st);
     delete h;
 }

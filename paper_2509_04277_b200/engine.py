@@ -205,18 +205,20 @@ class Engine:
         self._static_copy = ({a: np.array(getattr(self.world, a), copy=True)
                               for a in _STATIC_ATTRS} if self._small else None)
 
-    def _push(self):
-        """Host -> device before an epoch."""
+    def _push(self, state=True):
+        """Host -> device before an epoch.  Returns False when the World had
+        to be re-bound (everything, state included, is then uploaded);
+        state=False leaves the state to rs_run_epoch_host."""
         w = self.world
         if any(getattr(w, a) is not arr for a, arr in self._bound.items()):
             # an array attribute was replaced: re-bind (re-plans and uploads)
             self._bind()
-            return
+            return False
         static_dirty = w.static_version != self._static_version
         if self._small and not static_dirty:
             static_dirty = any(not np.array_equal(getattr(w, a), c)
                                for a, c in self._static_copy.items())
-        mask = _lib.RS_STATE | _lib.RS_CONTROL
+        mask = (_lib.RS_STATE if state else 0) | _lib.RS_CONTROL
         if static_dirty:
             mask |= _lib.RS_STATIC
             self._static_version = w.static_version
@@ -224,6 +226,7 @@ class Engine:
                 self._static_copy = {a: np.array(getattr(w, a), copy=True)
                                      for a in _STATIC_ATTRS}
         self._dev.upload(mask)
+        return True
 
     # -- commands ----------------------------------------------------------
 
@@ -313,9 +316,11 @@ class Engine:
         with self._lock:
             t0 = time.perf_counter_ns()
             self._drain_at_boundary()
-            self._push()
-            contacts, barrier_ns = self._dev.run(steps)
-            self._dev.download(_lib.RS_STATE)
+            if self._push(state=False):
+                contacts, barrier_ns = self._dev.run_host(steps)
+            else:   # re-bound: the state was just uploaded
+                contacts, barrier_ns = self._dev.run(steps)
+                self._dev.download(_lib.RS_STATE)
             self.world.step_index += steps
             self._resolve_applied()
             self.last_contacts = contacts
