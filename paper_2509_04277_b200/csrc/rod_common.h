@@ -72,6 +72,15 @@ struct DrvEntry {
 // and prefetching the next rod's state with TMA bulk copies (batches).
 enum Tier : int { TIER_CTA = 0, TIER_CLUSTER = 1, TIER_GRID = 2, TIER_STREAM = 3 };
 
+// Element material constants of a launch whose elements all share them
+// (batches of identical rods): passed by value in the kernel parameters, so
+// the step reads them as constant-bank operands instead of registers.
+template <typename Real>
+struct UniConsts {
+    Real l, il, kpl, ks, gt, gr;   // rest length, 1/l, K_p l, K_s, gamma_t, gamma_r
+    Real kb[3], us[3], I[3], rI[3];  // bend/twist stiffness, u*, inertia, 1/inertia
+};
+
 // Kernel arguments; device pointers, AoS layouts identical to world.py.
 template <typename Real>
 struct StepArgs {
@@ -103,6 +112,7 @@ struct StepArgs {
     int32_t any_grabs;                             //   barrier count must be uniform)
     int32_t ntasks;                                // stream tier: tasks for gridDim CTAs
     Real dt, beta, gx, gy, gz;
+    UniConsts<Real> u;                             // UNI == 2 launches
 };
 
 constexpr int PROF_SLOTS = 64;

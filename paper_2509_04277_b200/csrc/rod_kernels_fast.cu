@@ -6,10 +6,10 @@
 
 namespace rsb {
 namespace fast {
-template cudaError_t launch_step<float>(int, int, bool, const StepArgs<float>&, int, int, size_t, int, cudaStream_t);
-template cudaError_t launch_step<double>(int, int, bool, const StepArgs<double>&, int, int, size_t, int, cudaStream_t);
-template cudaError_t occupancy<float>(int, int, bool, int, size_t, int, int*);
-template cudaError_t occupancy<double>(int, int, bool, int, size_t, int, int*);
+template cudaError_t launch_step<float>(int, int, int, const StepArgs<float>&, int, int, size_t, int, cudaStream_t);
+template cudaError_t launch_step<double>(int, int, int, const StepArgs<double>&, int, int, size_t, int, cudaStream_t);
+template cudaError_t occupancy<float>(int, int, int, int, size_t, int, int*);
+template cudaError_t occupancy<double>(int, int, int, int, size_t, int, int*);
 
 // Issue-rate microbenchmark for the compute cross-check of the roofline:
 // `kind` 0 = DFMA, 1 = DADD, 2 = DMUL, 3 = FFMA; 8 independent chains per

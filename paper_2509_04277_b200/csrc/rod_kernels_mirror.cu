@@ -7,8 +7,8 @@
 
 namespace rsb {
 namespace mirror {
-template cudaError_t launch_step<double>(int, int, bool, const StepArgs<double>&, int, int, size_t, int, cudaStream_t);
-template cudaError_t occupancy<double>(int, int, bool, int, size_t, int, int*);
+template cudaError_t launch_step<double>(int, int, int, const StepArgs<double>&, int, int, size_t, int, cudaStream_t);
+template cudaError_t occupancy<double>(int, int, int, int, size_t, int, int*);
 }  // namespace mirror
 }  // namespace rsb
 

@@ -19,9 +19,10 @@ namespace RSB_MODE_NS {
 // room for the tail slot.
 //   V0 (1,132)  V1 (1,258)  V2 (1,514)  V3 (2,770)  V4 (4,1154)
 //   V5 (1,130) and V6 (2,130): batches of 129-point rods, 5 CTAs per SM
+//   V7 (2,136): the same without the TMA staging buffer, 8 CTAs per SM
 // Cluster tier: V0, V1, V2, V4; grid tier: V2, V4.
 
-template <typename Real, int S, int CAP, int TIER, bool UNI>
+template <typename Real, int S, int CAP, int TIER, int UNI>
 static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
                               size_t smem, int cluster, cudaStream_t st) {
     auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
@@ -59,7 +60,7 @@ static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
     }
 }
 
-template <typename Real, int S, int CAP, int TIER, bool UNI>
+template <typename Real, int S, int CAP, int TIER, int UNI>
 static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out) {
     auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -90,18 +91,23 @@ static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out
 }
 
 // what: 0 = launch, 1 = occupancy query
+// uni: 0 per-slot constants, 1 CTA-uniform (registers), 2 launch-uniform
+// (kernel parameters)
 template <typename Real, int S, int CAP, int TIER>
-static cudaError_t dispatch_uni(int what, bool uni, const StepArgs<Real>* a, int ncta, int threads,
+static cudaError_t dispatch_uni(int what, int uni, const StepArgs<Real>* a, int ncta, int threads,
                                 size_t smem, int cluster, cudaStream_t st, int* out) {
-    if (what == 0)
-        return uni ? launch_one<Real, S, CAP, TIER, true>(*a, ncta, threads, smem, cluster, st)
-                   : launch_one<Real, S, CAP, TIER, false>(*a, ncta, threads, smem, cluster, st);
-    return uni ? occupancy_one<Real, S, CAP, TIER, true>(threads, smem, cluster, out)
-               : occupancy_one<Real, S, CAP, TIER, false>(threads, smem, cluster, out);
+    if (what == 0) {
+        if (uni == 2) return launch_one<Real, S, CAP, TIER, 2>(*a, ncta, threads, smem, cluster, st);
+        if (uni == 1) return launch_one<Real, S, CAP, TIER, 1>(*a, ncta, threads, smem, cluster, st);
+        return launch_one<Real, S, CAP, TIER, 0>(*a, ncta, threads, smem, cluster, st);
+    }
+    if (uni == 2) return occupancy_one<Real, S, CAP, TIER, 2>(threads, smem, cluster, out);
+    if (uni == 1) return occupancy_one<Real, S, CAP, TIER, 1>(threads, smem, cluster, out);
+    return occupancy_one<Real, S, CAP, TIER, 0>(threads, smem, cluster, out);
 }
 
 template <typename Real>
-static cudaError_t dispatch(int what, int variant, int tier, bool uni, const StepArgs<Real>* a,
+static cudaError_t dispatch(int what, int variant, int tier, int uni, const StepArgs<Real>* a,
                             int ncta, int threads, size_t smem, int cluster, cudaStream_t st,
                             int* out) {
 #define RSB_D(S, CAP, TIER) dispatch_uni<Real, S, CAP, TIER>(what, uni, a, ncta, threads, smem, cluster, st, out)
@@ -114,11 +120,13 @@ static cudaError_t dispatch(int what, int variant, int tier, bool uni, const Ste
             case 4: return RSB_D(4, 1154, TIER_CTA);
             case 5: return RSB_D(1, 130, TIER_CTA);
             case 6: return RSB_D(2, 130, TIER_CTA);
+            case 7: return RSB_D(2, 136, TIER_CTA);
         }
     } else if (tier == TIER_STREAM) {
         switch (variant) {
             case 5: return RSB_D(1, 130, TIER_STREAM);
             case 6: return RSB_D(2, 130, TIER_STREAM);
+            case 7: return RSB_D(2, 136, TIER_STREAM);
         }
     } else if (tier == TIER_CLUSTER) {
         switch (variant) {
@@ -138,13 +146,13 @@ static cudaError_t dispatch(int what, int variant, int tier, bool uni, const Ste
 }
 
 template <typename Real>
-cudaError_t launch_step(int variant, int tier, bool uni, const StepArgs<Real>& a, int ncta,
+cudaError_t launch_step(int variant, int tier, int uni, const StepArgs<Real>& a, int ncta,
                         int threads, size_t smem, int cluster, cudaStream_t st) {
     return dispatch<Real>(0, variant, tier, uni, &a, ncta, threads, smem, cluster, st, nullptr);
 }
 
 template <typename Real>
-cudaError_t occupancy(int variant, int tier, bool uni, int threads, size_t smem, int cluster, int* out) {
+cudaError_t occupancy(int variant, int tier, int uni, int threads, size_t smem, int cluster, int* out) {
     return dispatch<Real>(1, variant, tier, uni, nullptr, 0, threads, smem, cluster, nullptr, out);
 }
 

@@ -28,15 +28,15 @@
 namespace rsb {
 namespace mirror {
 template <typename Real>
-cudaError_t launch_step(int, int, bool, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
+cudaError_t launch_step(int, int, int, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
 template <typename Real>
-cudaError_t occupancy(int, int, bool, int, size_t, int, int*);
+cudaError_t occupancy(int, int, int, int, size_t, int, int*);
 }  // namespace mirror
 namespace fast {
 template <typename Real>
-cudaError_t launch_step(int, int, bool, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
+cudaError_t launch_step(int, int, int, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
 template <typename Real>
-cudaError_t occupancy(int, int, bool, int, size_t, int, int*);
+cudaError_t occupancy(int, int, int, int, size_t, int, int*);
 }  // namespace fast
 }  // namespace rsb
 
@@ -71,11 +71,17 @@ struct Variant {
 };
 // capacity-ordered variants 0..4, then the batched variants 5 (strided, 128
 // threads) and 6 (paired, 64 threads) for 129-point rods
-constexpr Variant kVariants[] = {{1, 132}, {1, 258}, {1, 514}, {2, 770}, {4, 1154}, {1, 130}, {2, 130}};
-constexpr int kNumVariants = 7;
+constexpr Variant kVariants[] = {{1, 132}, {1, 258}, {1, 514}, {2, 770}, {4, 1154}, {1, 130}, {2, 130}, {2, 136}};
+constexpr int kNumVariants = 8;
 constexpr int kNumCapVariants = 5;
-constexpr int kBatchVariant = 5;
-constexpr int kClusterVariant = 4;
+constexpr int kBatchVariant = 7;   // batches of short rods; 5 and 6 on request
+// Cluster CTAs, smallest first: a rod (or bound set) above kCtaMaxPoints is
+// spread over as many CTAs (<= 16) of the smallest of these as it needs.
+// Measured (profiles/, cfg4 N = 1024): one 256-thread CTA 24.7 us/step, a
+// 9-CTA cluster of 128-point CTAs 13.8 us/step -- below ~512 points the
+// cluster barrier (~300 ns) costs more than the single CTA's extra work.
+constexpr int kClusterVariants[] = {0, 1, 2, 4};
+constexpr int kCtaMaxPoints = 513;   // variant 2 covers 512 slots + the tail
 constexpr int kMaxCluster = 16;
 constexpr int kRingCap = 64;
 constexpr int kMaxStepsPerLaunch = 1 << 16;
@@ -89,7 +95,8 @@ struct Segment {     // consecutive rods that must share a CTA / cluster / grid
 struct Group {       // one kernel launch
     int tier = TIER_CTA;
     int variant = 0;
-    bool uni = false;
+    int uni = 0;                    // constants: 0 per slot, 1 per CTA, 2 per launch
+    int32_t e_launch = 0;           // element standing for the launch (uni == 2)
     int task_begin = 0, ncta = 0;   // tasks (one CTA each, except stream)
     int grid = 0;                   // CTAs launched (stream: persistent)
     int threads = 0;
@@ -247,7 +254,7 @@ int64_t rod_of(const rs_world_desc& d, int64_t p) {
 
 // ---- launch planning --------------------------------------------------------
 
-int occupancy_query(rs_handle h, int variant, int tier, bool uni, int threads, size_t smem,
+int occupancy_query(rs_handle h, int variant, int tier, int uni, int threads, size_t smem,
                     int cluster, int* out) {
     cudaError_t e;
     if (h->prec == RS_F64_MIRROR)
@@ -346,12 +353,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     }
 
     // -- choose tiers --------------------------------------------------------
-    const int cta_cap = kVariants[kNumCapVariants - 1].cover();
+    const int cta_cap = d.force_tier == TIER_CTA ? kVariants[kNumCapVariants - 1].cover() : kCtaMaxPoints;
+    const int clu_cap = kVariants[kNumCapVariants - 1].cover();
     std::vector<int> seg_tier(segs.size());
     int64_t max_cta_seg = 0;
     for (size_t i = 0; i < segs.size(); ++i) {
         const int64_t np = segs[i].p1 - segs[i].p0;
-        int tier = np <= cta_cap ? TIER_CTA : (np <= int64_t(kMaxCluster) * cta_cap ? TIER_CLUSTER : TIER_GRID);
+        int tier = np <= cta_cap ? TIER_CTA : (np <= int64_t(kMaxCluster) * clu_cap ? TIER_CLUSTER : TIER_GRID);
         if (d.force_tier >= 0) tier = d.force_tier;
         if (tier == TIER_CTA && np > cta_cap)
             return fail(RS_E_INVALID, "segment of %lld points does not fit one CTA", (long long)np);
@@ -442,7 +450,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         const int64_t np = segs[i].p1 - segs[i].p0;
         Group g;
         g.tier = seg_tier[i];
-        g.variant = kClusterVariant;
+        g.variant = 4;
+        if (g.tier == TIER_CLUSTER)
+            for (int v : kClusterVariants)
+                if ((np + kVariants[v].cover() - 1) / kVariants[v].cover() <= kMaxCluster) {
+                    g.variant = v;
+                    break;
+                }
         if (d.force_variant >= 0 && d.force_variant <= 4 && d.force_variant != 3 &&
             (g.tier == TIER_CLUSTER || d.force_variant == 2 || d.force_variant == 4))
             g.variant = d.force_variant;
@@ -558,7 +572,8 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     // -- per-launch uniformity, sizes and occupancy checks -------------------
     for (Group& g : h->groups) {
         const Variant var = kVariants[g.variant];
-        bool uni = true;
+        bool uni = true, launch_uni = true;   // per CTA / across the whole launch
+        int64_t g_e0 = -1;
         int max_np = 0, bcap = 0, dcap = 0;
         for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
             CtaTask& tk = h->h_tasks[t];
@@ -575,8 +590,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                 }
             }
             tk.e_uni = int32_t(std::max<int64_t>(e0, 0));
+            if (e0 >= 0) {
+                if (g_e0 < 0) g_e0 = e0;
+                else if (launch_uni && !elem_consts_equal(d, g_e0, e0)) launch_uni = false;
+            }
         }
-        g.uni = uni;
+        g.uni = uni ? (launch_uni && g_e0 >= 0 ? 2 : 1) : 0;
+        g.e_launch = int32_t(std::max<int64_t>(g_e0, 0));
         g.bind_cap = bcap;
         g.drv_cap = std::max(dcap, 1);
         // slots the threads must cover: a task whose last slot is a rod end
@@ -594,14 +614,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                         var.CAP, max_np);
         // batches of whole single rods with no bindings: persistent stream
         // tier (TMA prefetch of the next rod while the current one steps)
-        if (g.tier == TIER_CTA && (g.variant == kBatchVariant || g.variant == kBatchVariant + 1) &&
-            d.force_tier < 0) {
+        if (g.tier == TIER_CTA && g.variant >= 5 && d.force_tier < 0) {
             bool single = true;
             for (int t = g.task_begin; t < g.task_begin + g.ncta && single; ++t)
                 single = h->h_tasks[t].nrods == 1 && h->h_tasks[t].bind_count == 0;
             if (single) g.tier = TIER_STREAM;
         }
-        const bool stream = g.tier == TIER_STREAM;
+        const bool stream = g.tier == TIER_STREAM && stream_staged(var.S, var.CAP);
         size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap, stream).total
                                         : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap, stream).total;
         const int stage_cap = BIND_FIELDS * var.CAP / BIND_REALS;
@@ -832,6 +851,22 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
         a.any_binds |= h->h_tasks[t].bind_count > 0;
         a.any_grabs |= h->h_tasks[t].grab_count > 0;
+    }
+    if (g.uni == 2) {   // the same arithmetic the kernel's load_elem_consts does
+        const int64_t e = g.e_launch;
+        const rs_world_desc& d = h->d;
+        a.u.l = Real(d.rest[e]);
+        a.u.il = Real(1.0) / a.u.l;
+        a.u.kpl = Real(d.kp[e]) * a.u.l;
+        a.u.ks = Real(d.ks[e]);
+        a.u.gt = Real(d.gt[e]);
+        a.u.gr = Real(d.gr[e]);
+        for (int k = 0; k < 3; ++k) {
+            a.u.kb[k] = Real(d.kb[3 * e + k]);
+            a.u.us[k] = Real(d.ustar[3 * e + k]);
+            a.u.I[k] = Real(d.inert[3 * e + k]);
+            a.u.rI[k] = Real(1.0) / a.u.I[k];
+        }
     }
     a.dt = Real(h->d.dt);
     a.beta = Real(h->d.beta);
@@ -1249,7 +1284,7 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "
                  "\"uniform\": %s, \"ctas\": %d, \"grid\": %d, \"threads\": %d, \"cluster\": %d, "
                  "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d}",
-                 i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni ? "true" : "false", g.ncta,
+                 i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni == 2 ? "\"launch\"" : (g.uni ? "true" : "false"), g.ncta,
                  g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap);
         s += tmp;
     }

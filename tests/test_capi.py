@@ -77,18 +77,23 @@ def test_plan_single_rods_by_size():
 
 def test_plan_pair_keeps_bound_rods_together_with_parallel_bindings():
     g = plan(wl.pair())
-    assert len(g) == 1 and g[0]["tier"] == "cta" and g[0]["points"] == 1026
-    assert g[0]["bind_cap"] == 513          # a matching: one binding per thread slot
+    # both rods in one 9-CTA cluster of 128-point CTAs (1026 points)
+    assert len(g) == 1 and g[0]["tier"] == "cluster" and g[0]["points"] == 1026
+    assert g[0]["ctas"] == 9 and g[0]["cluster"] == 9
+    # a matching: each binding applied in parallel by the CTA owning point a
+    assert 0 < g[0]["bind_cap"] <= 128
+    g = plan(wl.pair(), force_tier=0)
+    assert g[0]["tier"] == "cta" and g[0]["bind_cap"] == 513
 
 
 def test_plan_batched_rods_use_occupancy_variant():
     g = plan(wl.hair(2048))[0]
-    # persistent stream tier: 2048 rod tasks over <= 5 CTAs per SM; a
-    # 129-point rod is 128 threads plus the tip as thread 0's tail slot
-    assert g["tier"] == "stream" and g["variant"] == 5 and g["ctas"] == 2048
-    assert g["threads"] == 128 and g["grid"] <= 5 * 148
-    paired = plan(wl.hair(2048), force_variant=6)[0]
-    assert paired["tier"] == "stream" and paired["threads"] == 64
+    # persistent stream tier: 2048 rod tasks over <= 8 CTAs per SM; a
+    # 129-point rod is 64 threads x 2 slots plus the tip as thread 0's tail
+    assert g["tier"] == "stream" and g["variant"] == 7 and g["ctas"] == 2048
+    assert g["threads"] == 64 and g["grid"] <= 8 * 148
+    strided = plan(wl.hair(2048), force_variant=5)[0]
+    assert strided["tier"] == "stream" and strided["threads"] == 128
     small = plan(wl.hair(16))[0]
     assert small["tier"] == "cta"
 

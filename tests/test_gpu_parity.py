@@ -131,7 +131,7 @@ def test_cfg5_hair_sample_bitwise():
     parity(lambda: wl.hair(16), 200, 50)
 
 
-@pytest.mark.parametrize("k,variant", [(1, 5), (7, 5), (1, 6), (7, 6)])
+@pytest.mark.parametrize("k,variant", [(1, 5), (7, 5), (1, 6), (7, 6), (1, 7), (7, 7)])
 def test_cfg5_stream_tier_bitwise(k, variant):
     # enough rods for the persistent TMA-prefetch stream tier
     def make():
@@ -183,7 +183,7 @@ def test_cluster_pair_overlapping_bindings_sequential_bitwise():
     parity(make, 60, 20, force_tier=1, force_ctas=3)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 def test_cta_variants_bitwise(variant):
     parity(lambda: wl.cantilever(100, 0.2), 100, 50, force_variant=variant)
 
