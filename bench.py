@@ -75,13 +75,58 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+# fp64 pipe instructions the fp64 mirror kernel issues per slot-step (ncu SASS
+# count, DADD + DMUL + DFMA, profiles/r01_ncu_*): the compute cross-check
+FP64_INST_PER_SLOT_STEP = 715
+
+
+def fp64_peak():
+    """Measured DADD issue rate (ops/s) on this device (rs_pipe_peak)."""
+    from paper_2509_04277_b200 import _lib
+    try:
+        return _lib.pipe_peak(1)
+    except Exception:
+        return None
+
+
+def pcie_bidir_gbs(nbytes=256 << 20):
+    """Pinned host <-> device bandwidth with both directions in flight (the
+    e2e path's bound: every epoch moves the full state both ways)."""
+    import torch
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_b, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+    both()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(4):
+        both()
+    e1.record()
+    torch.cuda.synchronize()
+    return 2 * 4 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+
 def load_traffic(key):
+    """(dram bytes read + written per launch, source) from the committed
+    ncu --set full capture of the same workload, or (None, None)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(key)
+            t = json.load(fh).get(key)
+        return float(t["bytes"]), t["source"]
     except Exception:
-        return None
+        return None, None
 
 
 # ---- clocks sampled during the timed region --------------------------------
@@ -237,6 +282,24 @@ class _CudaArray:
 
 # ---- single-rod latency measurements (rank 0, N = 1) ------------------------
 
+def barrier_ns(plan):
+    """Measured cost of one phase barrier of a plan's tier (rs_micro)."""
+    from paper_2509_04277_b200 import _lib
+    if plan["tier"] in ("cluster", "grid"):
+        return _lib.micro("cluster_barrier", max(2, min(16, plan["ctas"])))[1]
+    return _lib.micro("bar_sync", plan["threads"])[1]
+
+
+def latency_floor(plan, us, iters=10, binds=False):
+    """Synchronisation floor of one step: n_sync phase barriers (2I+3, 3I+3
+    with bindings) at the measured barrier latency of
+    the tier -- t_floor without the per-phase dependency chains."""
+    n_sync = (3 if binds else 2) * iters + 3
+    floor = n_sync * barrier_ns(plan) / 1e3
+    return {"n_sync": n_sync, "barrier_ns": barrier_ns(plan), "sync_floor_us": floor,
+            "frac": floor / us}
+
+
 def single_rod_suite(precision):
     from paper_2509_04277_b200 import workloads as wl
     from paper_2509_04277_b200.engine import Engine
@@ -259,12 +322,14 @@ def single_rod_suite(precision):
     us, plan = device_us(wl.cantilever, 1000, 3)
     cpu, kind = cpu_single_rod_us(wl.cantilever, 1000)
     out["cfg1_cantilever_64"] = {"us_per_step": us, "k": 1000, "tier": plan["tier"],
-                                 "cpu_us_per_step": cpu, "cpu_kind": kind}
+                                 "cpu_us_per_step": cpu, "cpu_kind": kind,
+                                 "roofline": latency_floor(plan, us)}
     us, plan = device_us(wl.extensible, 10, 100)
     cpu, _ = cpu_single_rod_us(wl.extensible, 200)
     out["cfg2_extensible_512"] = {"us_per_step": us, "k": 10, "tier": plan["tier"],
-                                  "cpu_us_per_step": cpu}
+                                  "cpu_us_per_step": cpu, "roofline": latency_floor(plan, us)}
     us, plan = device_us(wl.pair, 10, 100)
+    pair_plan = plan
     cpu, _ = cpu_single_rod_us(wl.pair, 100)
     # haptic frame loop: commands in, K = 10 steps (1 ms simulated), state out
     w = wl.pair()
@@ -280,8 +345,9 @@ def single_rod_suite(precision):
             _ = float(tip[2])
     frames = np.array(frames[100:]) * 1e6
     out["cfg3_pair_2x512"] = {
-        "us_per_step": us, "k": 10, "tier": plan["tier"], "steps_per_s": 1e6 / us,
-        "cpu_us_per_step": cpu,
+        "us_per_step": us, "k": 10, "tier": pair_plan["tier"], "ctas": pair_plan["ctas"],
+        "steps_per_s": 1e6 / us, "cpu_us_per_step": cpu,
+        "roofline": latency_floor(pair_plan, us, binds=True),
         "haptic_frame_us": {"median": float(np.median(frames)),
                             "p99": float(np.percentile(frames, 99)),
                             "frames": int(frames.size),
@@ -295,6 +361,7 @@ def single_rod_suite(precision):
             row[f"k{k}"] = us
         row["tier"] = plan["tier"]
         row["ctas"] = plan["ctas"]
+        row["roofline_k100"] = latency_floor(plan, row["k100"])
         row["cpu_us_per_step"], _ = cpu_single_rod_us(lambda: wl.sweep(n),
                                                       max(3, 20000 // n))
         sweep[str(n)] = row
@@ -344,6 +411,19 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def compute_roofline(rods, launch_ms, precision):
+    """fp64 pipe cross-check: issued fp64 instructions (ncu count per
+    slot-step) per second against the measured DADD issue peak."""
+    if precision == "f32":
+        return None
+    peak = fp64_peak()
+    slots = rods * (ELEMENTS + 1)
+    achieved = FP64_INST_PER_SLOT_STEP * slots / (launch_ms * 1e-3)
+    return {"pipe": "fp64", "achieved": achieved, "peak": peak, "unit": "inst/s",
+            "frac": (achieved / peak) if peak else None,
+            "inst_per_slot_step": FP64_INST_PER_SLOT_STEP}
+
+
 def run_ours(args):
     world, rank, local = dist_env()
     D = Dist(world, rank, local)
@@ -386,7 +466,7 @@ def run_ours(args):
     bytes_per_launch = per * algorithmic_bytes_per_rod(ELEMENTS + 1, ELEMENTS, real)
     peak, peak_src = load_peaks()
     achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
-    traffic = load_traffic(f"hair_{args.precision}_k{args.k}_r{per}")
+    traffic, traffic_src = load_traffic(f"hair_{args.precision}_k{args.k}_r{per}")
 
     # ---- e2e through the public API (host numpy arrays) --------------
     state_bytes = 8 * (6 * P + 7 * E)
@@ -400,6 +480,18 @@ def run_ours(args):
     e2e_s = time.perf_counter() - t0
     e2e_max = D.max(e2e_s)
     e2e_value = args.rods * ELEMENTS * args.k * args.e2e_steps / e2e_max
+    pcie = pcie_bidir_gbs() if rank == 0 else None
+    e2e_gbs = (state_bytes * 2 + control_bytes) * args.e2e_steps / e2e_max / 1e9
+
+    # the same batch at K = 10 steps per launch (state stays on chip)
+    dev.run(10)
+    dev.synchronize()
+    dev.timer_start()
+    for _ in range(3):
+        dev.run(10)
+    dev.timer_stop()
+    ms10 = D.max(dev.timer_ms())
+    value_k10 = args.rods * ELEMENTS * 30 / (ms10 * 1e-3)
 
     # ---- NCCL gather of the final positions (results only) -----------
     gathered = None
@@ -432,12 +524,17 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "element-steps/s",
                     "h2d_bytes_per_step": state_bytes + control_bytes,
                     "d2h_bytes_per_step": state_bytes,
-                    "steps": args.e2e_steps, "api": "Engine.run_epoch"},
+                    "steps": args.e2e_steps, "api": "Engine.run_epoch",
+                    "roofline": {"bound": "pcie", "achieved": e2e_gbs, "peak": pcie,
+                                 "unit": "GB/s", "frac": (e2e_gbs / pcie) if pcie else None,
+                                 "peak_source": "pinned H2D+D2H both in flight, measured in this run"}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
                          "bytes_per_launch": bytes_per_launch,
                          "launch_ms": launch_ms},
+            "compute_roofline": compute_roofline(per, launch_ms, args.precision),
+            "value_k10": value_k10,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "build_s": t_build,
