@@ -352,6 +352,16 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         r = end + 1;
     }
 
+    // the paired stream variants take colour p from slot parity p: every
+    // rod's element colours must alternate from its first element
+    bool colours_aligned = true;
+    for (int64_t r = 0; r < R && colours_aligned; ++r)
+        for (int64_t p = d.rod_offsets[r]; p < d.rod_offsets[r + 1] - 1; ++p)
+            if (((pflags[p] & SF_PARITY) != 0) != (((p - d.rod_offsets[r]) & 1) != 0)) {
+                colours_aligned = false;
+                break;
+            }
+
     // -- choose tiers --------------------------------------------------------
     const int cta_cap = d.force_tier == TIER_CTA ? kVariants[kNumCapVariants - 1].cover() : kCtaMaxPoints;
     const int clu_cap = kVariants[kNumCapVariants - 1].cover();
@@ -411,7 +421,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             if (seg_tier[i] == TIER_CTA) cta_points += segs[i].p1 - segs[i].p0;
         if (max_cta_seg <= kVariants[kBatchVariant].cover() + 1 &&
             cta_points >= int64_t(2) * kVariants[kBatchVariant].CAP * h->num_sms)
-            v = kBatchVariant;
+            v = colours_aligned ? kBatchVariant : 5;
         if (d.force_variant >= 0) {
             if (d.force_variant >= kNumVariants || kVariants[d.force_variant].cover() + 1 < max_cta_seg)
                 return fail(RS_E_INVALID, "force_variant %d cannot hold %lld points", d.force_variant,
@@ -614,7 +624,8 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                         var.CAP, max_np);
         // batches of whole single rods with no bindings: persistent stream
         // tier (TMA prefetch of the next rod while the current one steps)
-        if (g.tier == TIER_CTA && g.variant >= 5 && d.force_tier < 0) {
+        if (g.tier == TIER_CTA && g.variant >= 5 && d.force_tier < 0 &&
+            (colours_aligned || !paired(var.S))) {
             bool single = true;
             for (int t = g.task_begin; t < g.task_begin + g.ncta && single; ++t)
                 single = h->h_tasks[t].nrods == 1 && h->h_tasks[t].bind_count == 0;

@@ -150,6 +150,21 @@ def test_cfg5_stream_tier_bitwise(k, variant):
     assert_bitwise(g, r)
 
 
+def test_stream_tier_colours_not_from_slot_parity_bitwise():
+    # one rod's red/black colouring flipped: the paired (slot-parity) stream
+    # variants do not apply and the planner falls back to the strided one
+    def make():
+        w = wl.hair(1700)
+        o = w.rod_infos[5].point_offset - 5
+        w.elem_parity[o:o + 128] ^= 1
+        return w
+    g, r = make(), make()
+    plan = run_gpu(g, 12, 4)
+    assert plan["groups"][0]["tier"] == "stream" and plan["groups"][0]["variant"] == 5
+    OracleStepper(r).run(12)
+    assert_bitwise(g, r)
+
+
 # -- forced tiers on small rods (exercise DSMEM / halo paths cheaply) ---------
 
 @pytest.mark.parametrize("ctas", [2, 3, 5, 8, 16])
