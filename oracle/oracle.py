@@ -49,6 +49,13 @@ class RoWorld(ctypes.Structure):
         ("ef", _p), ("ff_own", _p), ("ff_next", _p), ("jtau", _p),
         ("pt_elo", _p), ("pt_ehi", _p),
         ("step", _i64), ("err_step", _i64),
+        ("has_mesh", _i64), ("n_nodes", _i64),
+        ("nmin", _p), ("nmax", _p), ("verts", _p),
+        ("nstart", _p), ("ncount", _p), ("torder", _p), ("tris", _p),
+        ("cradii", _p), ("cmask", _p), ("cact", _p), ("cnorm", _p), ("cdepth", _p),
+        ("cacc_n", _p), ("cacc_t", _p),
+        ("coll_interval", _i64), ("coll_margin", _f64), ("restitution", _f64), ("mu", _f64),
+        ("contacts", _i64),
     ]
 
 
@@ -62,7 +69,7 @@ def load_oracle():
             raise ImportError(f"{ORACLE_LIB} missing: run `make oracle/liboracle.so`")
         lib = ctypes.CDLL(ORACLE_LIB)
         for name in ("ro_prepare", "ro_scatter", "ro_gather", "ro_central",
-                     "ro_integrate"):
+                     "ro_contacts", "ro_integrate"):
             getattr(lib, name).argtypes = [ctypes.POINTER(RoWorld)]
             getattr(lib, name).restype = None
         lib.ro_run.argtypes = [ctypes.POINTER(RoWorld), _i64]
@@ -77,9 +84,8 @@ class OracleStepper:
     """Steps a World's arrays in place with the C restatement."""
 
     def __init__(self, world):
-        if getattr(world, "tree", None) is not None or getattr(
-                world, "self_collision_enabled", False):
-            raise NotImplementedError("oracle covers the hot-path scope only")
+        if getattr(world, "self_collision_enabled", False):
+            raise NotImplementedError("oracle does not cover self-collision")
         self.lib = load_oracle()
         self.world = w = world
         c = np.ascontiguousarray
@@ -109,7 +115,21 @@ class OracleStepper:
             "ff_next": np.zeros((E, 4)), "jtau": np.zeros((E, 3)),
             "pt_elo": np.zeros(P, dtype=np.int64),
             "pt_ehi": np.zeros(P, dtype=np.int64),
+            # contact slots are World state, stepped in place
+            "cradii": c(w.contact_radii), "cmask": c(w.collide_mesh_mask).view(np.uint8),
+            "cact": w.contact_active, "cnorm": w.contact_normal, "cdepth": w.contact_depth,
+            "cacc_n": w.contact_acc_n, "cacc_t": w.contact_acc_t,
         }
+        tree = getattr(w, "tree", None)
+        if tree is not None:
+            if tree.max_depth + 1 > 32:
+                raise RuntimeError("tree deeper than the traversal stack capacity")
+            self.keep.update({
+                "nmin": c(tree.node_min), "nmax": c(tree.node_max), "verts": c(tree.vertices),
+                "nstart": c(tree.node_start, dtype=np.int64),
+                "ncount": c(tree.node_count, dtype=np.int64),
+                "torder": c(tree.tri_order, dtype=np.int64),
+                "tris": c(tree.triangles, dtype=np.int64)})
         s = RoWorld()
         s.P, s.E, s.R = P, E, len(w.rod_infos)
         s.iters = w.solver.iterations
@@ -122,6 +142,12 @@ class OracleStepper:
         s.ngrab = self.keep["g_act"].shape[0]
         s.step = w.step_index
         s.err_step = -1
+        s.has_mesh = int(tree is not None)
+        s.n_nodes = tree.node_min.shape[0] if tree is not None else 0
+        s.coll_interval = int(w.collision_interval)
+        s.coll_margin = float(w.collision_margin)
+        s.restitution = float(w.solver.restitution)
+        s.mu = float(w.solver.mu)
         self.s = s
         self.lib.ro_prepare(ctypes.byref(s))
 
@@ -132,6 +158,11 @@ class OracleStepper:
     @property
     def error_step(self):
         return int(self.s.err_step)
+
+    @property
+    def contacts(self):
+        """Active mesh contacts after the last step (step_serial's return)."""
+        return int(self.s.contacts)
 
 
 # ---- the reference's own compiled core ---------------------------------------

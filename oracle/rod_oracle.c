@@ -169,10 +169,216 @@ static void scatter_element(ro_world *w, int64_t e)
         w->jtau[3 * e + k] = w->gr[e] * (w->w[3 * (e + 1) + k] - w->w[3 * e + k]);
 }
 
+/* ---- mesh contacts: detection (_core.pyx:509-662) ----------------------- */
+
+#define RO_STACK_CAP 32
+
+/* Ericson's closest point of triangle abc to p (_core.pyx:509-559) */
+static void closest_tri(const double *p, const double *a, const double *b, const double *c,
+                        double *out)
+{
+    double ab[3], ac[3], ap[3], bp[3], cp[3];
+    for (int k = 0; k < 3; ++k) {
+        ab[k] = b[k] - a[k];
+        ac[k] = c[k] - a[k];
+        ap[k] = p[k] - a[k];
+    }
+    const double d1 = ab[0] * ap[0] + ab[1] * ap[1] + ab[2] * ap[2];
+    const double d2 = ac[0] * ap[0] + ac[1] * ap[1] + ac[2] * ap[2];
+    if (d1 <= 0.0 && d2 <= 0.0) {
+        for (int k = 0; k < 3; ++k) out[k] = a[k];
+        return;
+    }
+    for (int k = 0; k < 3; ++k) bp[k] = p[k] - b[k];
+    const double d3 = ab[0] * bp[0] + ab[1] * bp[1] + ab[2] * bp[2];
+    const double d4 = ac[0] * bp[0] + ac[1] * bp[1] + ac[2] * bp[2];
+    if (d3 >= 0.0 && d4 <= d3) {
+        for (int k = 0; k < 3; ++k) out[k] = b[k];
+        return;
+    }
+    const double vc = d1 * d4 - d3 * d2;
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        const double t = d1 / (d1 - d3);
+        for (int k = 0; k < 3; ++k) out[k] = a[k] + t * ab[k];
+        return;
+    }
+    for (int k = 0; k < 3; ++k) cp[k] = p[k] - c[k];
+    const double d5 = ab[0] * cp[0] + ab[1] * cp[1] + ab[2] * cp[2];
+    const double d6 = ac[0] * cp[0] + ac[1] * cp[1] + ac[2] * cp[2];
+    if (d6 >= 0.0 && d5 <= d6) {
+        for (int k = 0; k < 3; ++k) out[k] = c[k];
+        return;
+    }
+    const double vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        const double t = d2 / (d2 - d6);
+        for (int k = 0; k < 3; ++k) out[k] = a[k] + t * ac[k];
+        return;
+    }
+    const double va = d3 * d6 - d5 * d4;
+    if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+        const double t = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        for (int k = 0; k < 3; ++k) out[k] = b[k] + t * (c[k] - b[k]);
+        return;
+    }
+    const double denom = 1.0 / (va + vb + vc);
+    for (int k = 0; k < 3; ++k) out[k] = a[k] + ab[k] * (vb * denom) + ac[k] * (vc * denom);
+}
+
+/* broad + narrow phase + aggregation for the sphere of point i */
+static void mesh_contact(ro_world *w, int64_t i)
+{
+    int64_t stack[RO_STACK_CAP];
+    const double *center = w->pos + 3 * i;
+    const double radius = w->cradii[i] + w->coll_margin;
+    double lo[3], hi[3], wsum[3] = {0.0, 0.0, 0.0}, best_n[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = center[k] - radius;
+        hi[k] = center[k] + radius;
+    }
+    int64_t nhits = 0, top = 1;
+    double maxd = -1.0;
+    stack[0] = 0;
+    while (top) {
+        const int64_t node = stack[--top];
+        if (node >= w->n_nodes || w->ncount[node] < 0)
+            continue;
+        const double *mn = w->nmin + 3 * node, *mx = w->nmax + 3 * node;
+        if (mn[0] > hi[0] || mn[1] > hi[1] || mn[2] > hi[2] || mx[0] < lo[0] || mx[1] < lo[1] ||
+            mx[2] < lo[2])
+            continue;
+        const int64_t cnt = w->ncount[node];
+        if (cnt == 0) {
+            stack[top] = 2 * node + 1;
+            stack[top + 1] = 2 * node + 2;
+            top += 2;
+            continue;
+        }
+        for (int64_t t = w->nstart[node]; t < w->nstart[node] + cnt; ++t) {
+            const int64_t tri = w->torder[t];
+            const double *a = w->verts + 3 * w->tris[3 * tri];
+            const double *b = w->verts + 3 * w->tris[3 * tri + 1];
+            const double *c = w->verts + 3 * w->tris[3 * tri + 2];
+            double e1[3], e2[3], face[3], closest[3], delta[3], n[3];
+            for (int k = 0; k < 3; ++k) {
+                e1[k] = b[k] - a[k];
+                e2[k] = c[k] - a[k];
+            }
+            face[0] = e1[1] * e2[2] - e1[2] * e2[1];
+            face[1] = e1[2] * e2[0] - e1[0] * e2[2];
+            face[2] = e1[0] * e2[1] - e1[1] * e2[0];
+            const double area2 = sqrt(face[0] * face[0] + face[1] * face[1] + face[2] * face[2]);
+            if (area2 == 0.0) {
+                w->err_step = w->step;
+                continue;
+            }
+            closest_tri(center, a, b, c, closest);
+            for (int k = 0; k < 3; ++k) delta[k] = center[k] - closest[k];
+            const double d = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
+            if (d >= radius)
+                continue;
+            double dot = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                n[k] = face[k] / area2;
+                dot += n[k] * (center[k] - a[k]);
+            }
+            if (dot < 0.0)
+                for (int k = 0; k < 3; ++k) n[k] = -n[k];
+            const double depth = radius - d;
+            nhits += 1;
+            for (int k = 0; k < 3; ++k) wsum[k] += depth * n[k];
+            if (depth > maxd) {
+                maxd = depth;
+                for (int k = 0; k < 3; ++k) best_n[k] = n[k];
+            }
+        }
+    }
+    if (nhits == 0)
+        return;
+    const double norm = sqrt(wsum[0] * wsum[0] + wsum[1] * wsum[1] + wsum[2] * wsum[2]);
+    if (norm < 1e-12 * (maxd > 1.0 ? maxd : 1.0)) {
+        for (int k = 0; k < 3; ++k) w->cnorm[3 * i + k] = best_n[k];
+    } else {
+        for (int k = 0; k < 3; ++k) w->cnorm[3 * i + k] = wsum[k] / norm;
+    }
+    maxd -= w->coll_margin;               /* the margin inflates detection only */
+    if (maxd < 0.0)
+        maxd = 0.0;
+    w->cdepth[i] = maxd;
+    w->cact[i] = 1;
+    w->contacts += 1;
+}
+
+/* contact slot reset + detection for every point (_core.pyx:730-741) */
+static void detect_contacts(ro_world *w)
+{
+    const int detect = w->step % w->coll_interval == 0;
+    w->contacts = 0;
+    for (int64_t i = 0; i < w->P; ++i) {
+        w->cacc_n[i] = 0.0;
+        w->cacc_t[i] = 0.0;
+        if (detect) {
+            w->cact[i] = 0;
+            if (w->has_mesh && w->cmask[i])
+                mesh_contact(w, i);
+        } else if (w->cact[i]) {
+            w->contacts += 1;
+        }
+    }
+}
+
 void ro_scatter(ro_world *w)
 {
+    if (w->cact)
+        detect_contacts(w);
     for (int64_t e = 0; e < w->E; ++e)
         scatter_element(w, e);
+}
+
+/* ---- contact impulses with accumulator and box friction (_core.pyx:906-947) */
+
+void ro_contacts(ro_world *w)
+{
+    if (!w->cact)
+        return;
+    for (int64_t i = 0; i < w->P; ++i) {
+        if (w->cact[i] != 1 || w->plock[i])
+            continue;
+        double *v = w->vel + 3 * i, n[3], vt[3];
+        const double m = w->mass[i];
+        double vn = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            n[k] = w->cnorm[3 * i + k];
+            vn += v[k] * n[k];
+        }
+        const double raw = m * (-vn * (1.0 + w->restitution) + w->beta * w->cdepth[i] / w->dt);
+        double new_acc = w->cacc_n[i] + raw;
+        if (new_acc < 0.0)
+            new_acc = 0.0;
+        const double applied = new_acc - w->cacc_n[i];
+        for (int k = 0; k < 3; ++k) v[k] += (applied / m) * n[k];
+        w->cacc_n[i] = new_acc;
+        if (w->mu > 0.0) {
+            double dot = 0.0, vt_norm = 0.0;
+            for (int k = 0; k < 3; ++k) dot += v[k] * n[k];
+            for (int k = 0; k < 3; ++k) {
+                vt[k] = v[k] - dot * n[k];
+                vt_norm += vt[k] * vt[k];
+            }
+            vt_norm = sqrt(vt_norm);
+            double cap = w->mu * new_acc - w->cacc_t[i];
+            if (cap < 0.0)
+                cap = 0.0;
+            double jt = m * vt_norm;
+            if (jt > cap)
+                jt = cap;
+            if (vt_norm > 0.0) {
+                const double scale = jt / (m * vt_norm);
+                for (int k = 0; k < 3; ++k) v[k] -= scale * vt[k];
+            }
+            w->cacc_t[i] += jt;
+        }
+    }
 }
 
 /* ---- point / frame gather and velocity update (_core.pyx:808-875) ----- */
@@ -339,6 +545,7 @@ void ro_run(ro_world *w, int64_t steps)
         for (int64_t it = 0; it < w->iters; ++it) {
             ro_distance(w, 0);
             ro_distance(w, 1);
+            ro_contacts(w);
             ro_central(w);
         }
         ro_integrate(w);

@@ -10,8 +10,8 @@
  * positions/velocities (P,3) f64 AoS, frames (E,4), angular velocities (E,3),
  * per-element material arrays, per-point/per-frame lock flags, drivers,
  * bindings and grab anchors.  The stepping semantics follow the reference's
- * compiled serial step (_core.pyx:1058-1080) restricted to the hot-path scope:
- * no mesh contacts and no self-collision (SURVEY.md §8(f) "next").
+ * compiled serial step (_core.pyx:1058-1080): elastic forces, constraints,
+ * bindings, grabs and mesh contacts; no self-collision.
  */
 #ifndef ROD_ORACLE_H
 #define ROD_ORACLE_H
@@ -55,6 +55,19 @@ typedef struct ro_world {
     /* counters: step counter and last error step (-1 if none) */
     int64_t step;
     int64_t err_step;
+    /* mesh contacts (_core.pyx:509-662, 906-947); has_mesh 0: none.  The
+       tree arrays follow bvh.TriMeshBvh, the contact slots world.py:157-161 */
+    int64_t has_mesh, n_nodes;
+    const double *nmin, *nmax, *verts;
+    const int64_t *nstart, *ncount, *torder, *tris;
+    const double *cradii;        /* (P) contact radius */
+    const uint8_t *cmask;        /* (P) point collides with the mesh */
+    uint8_t *cact;               /* (P) contact active */
+    double *cnorm, *cdepth;      /* (P,3), (P) */
+    double *cacc_n, *cacc_t;     /* (P) impulse accumulators */
+    int64_t coll_interval;
+    double coll_margin, restitution, mu;
+    int64_t contacts;            /* active contacts after the last step */
 } ro_world;
 
 /* Build pt_elo / pt_ehi from elem_point (make_context, _core.pyx:264-272). */
@@ -66,6 +79,7 @@ void ro_scatter(ro_world *w);
 void ro_gather(ro_world *w);
 void ro_distance(ro_world *w, int64_t parity);
 void ro_central(ro_world *w);
+void ro_contacts(ro_world *w);
 void ro_integrate(ro_world *w);
 
 #ifdef __cplusplus

@@ -6,6 +6,8 @@ cfg3 `pair`        catheter/guidewire pair 2 x 512, bidirectional bindings,
                    both bases driven at 5 cm/s, I = 10
 cfg4 `sweep`       single inextensible rod of N elements, l = 2 mm
 cfg5 `hair`        R rods x 128 elements, roots clamped, random directions
+`insertion`        guidewire pushed into a curved tube mesh (mesh contacts)
+`floor_drop`       rod dropped onto a floor mesh (contacts + friction)
 
 All use the scenario material defaults (scenarios.py:30-32): r = 1 mm,
 E_s = 1e7, E_b = G = 1e6, rho = 0.05 kg/m, K_p = 1, gamma_t = 2e-4,
@@ -112,5 +114,37 @@ def shard(total_rods, world_size, rank):
     return rank * per, per
 
 
+def insertion(points=128, length=0.3, speed=0.05, tube=None):
+    """Paper insertion scene (scenarios.py:45-53): a guidewire pushed at its
+    base into a curved tube (meshes.curved_tube), mesh contacts detected
+    every 4th step with a 0.5 mm margin.  `tube` overrides the tube mesh
+    parameters (smaller tubes for quick tests)."""
+    from . import bvh, meshes
+    w = _world()
+    w.add_rod(st.init_rod(points, length, axis=(0.0, 0.0, 1.0), origin=(0.0, 0.0, -length)),
+              st.RodParams(**MATERIAL))
+    w.finalize()
+    w.set_mesh(bvh.build_aabb_tree(*meshes.curved_tube(**(tube or {}))))
+    w.collision_interval = 4
+    w.collision_margin = 5e-4
+    w.set_driver(0)
+    w.driver_velocity[0] = (0.0, 0.0, speed)
+    return w
+
+
+def floor_drop(points=33, length=0.2, height=0.02, restitution=0.0, mu=0.3):
+    """A horizontal rod dropped onto a floor grid (meshes.floor_mesh) with a
+    1 cm contact radius: contact detection, normal impulses and friction."""
+    from . import bvh, meshes
+    w = World(dt=1e-4, gravity=(0.0, -9.81, 0.0),
+              solver=SolverConfig(iterations=10, restitution=restitution, mu=mu))
+    w.add_rod(st.init_rod(points, length, axis=(1.0, 0.0, 0.2), origin=(-0.1, height, 0.0)),
+              st.RodParams(**MATERIAL), contact_radius=0.01)
+    w.finalize()
+    w.set_mesh(bvh.build_aabb_tree(*meshes.floor_mesh(size=0.3, cells=6)))
+    w.velocities[:] = (0.05, -0.5, 0.0)
+    return w
+
+
 BUILDERS = {"cantilever": cantilever, "extensible": extensible, "pair": pair,
-            "sweep": sweep, "hair": hair}
+            "sweep": sweep, "hair": hair, "insertion": insertion, "floor_drop": floor_drop}
