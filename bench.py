@@ -352,6 +352,12 @@ def single_rod_suite(precision):
                             "p99": float(np.percentile(frames, 99)),
                             "frames": int(frames.size),
                             "rate_hz_median": float(1e6 / np.median(frames))}}
+    # the paper's insertion scene: mesh contacts
+    us, plan = device_us(wl.insertion, 100, 10)
+    cpu, _ = cpu_single_rod_us(wl.insertion, 200)
+    out["insertion_128_tube"] = {"us_per_step": us, "k": 100, "tier": plan["tier"],
+                                 "cpu_us_per_step": cpu, "roofline": latency_floor(plan, us),
+                                 "mesh_triangles": 15360, "collision_interval": 4}
     sweep = {}
     for n in (16, 64, 256, 1024, 4096, 16384):
         row = {}

@@ -38,14 +38,15 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 
 enum rs_status {
     RS_OK = 0,
     RS_E_INVALID = -1,      /* bad argument (ValueError) */
     RS_E_CUDA = -2,         /* CUDA runtime failure (RuntimeError) */
     RS_E_UNSUPPORTED = -3,  /* scene feature outside this build's scope */
-    RS_E_RING_FULL = -4     /* command ring full (RuntimeError) */
+    RS_E_RING_FULL = -4,    /* command ring full (RuntimeError) */
+    RS_E_RUNTIME = -5       /* scene rejected at bind time (RuntimeError) */
 };
 
 enum rs_precision {
@@ -90,6 +91,23 @@ typedef struct rs_world_desc {
     uint8_t *g_act;
     int64_t *g_pt;
     double *g_tgt;                    /* (ngrab,3) */
+    /* mesh contacts (ABI 2).  The tree is the reference's TriMeshBvh
+     * (bvh.py:22-44): implicit-heap AABB nodes, <= 2 triangles per leaf;
+     * has_mesh 0 leaves the tree pointers unused.  The contact slots
+     * (world.py:157-161) are state: uploaded / downloaded with RS_STATE. */
+    int64_t has_mesh, n_nodes, mesh_depth, n_tris, n_verts;
+    const double *nmin, *nmax;        /* (n_nodes,3) node boxes */
+    const int64_t *nstart, *ncount;   /* (n_nodes) leaf range / count (-1 unused) */
+    const int64_t *torder, *tris;     /* (n_tris) leaf order, (n_tris,3) */
+    const double *verts;              /* (n_verts,3) */
+    const double *cradii;             /* (P) world.contact_radii */
+    const uint8_t *cmask;             /* (P) world.collide_mesh_mask */
+    uint8_t *cact;                    /* (P) contact_active */
+    double *cnorm, *cdepth;           /* (P,3) (P) contact_normal / depth */
+    double *cacc_n, *cacc_t;          /* (P) contact_acc_n / acc_t */
+    int64_t coll_interval;            /* world.collision_interval */
+    double coll_margin;               /* world.collision_margin */
+    double restitution, mu;           /* solver.restitution, solver.mu */
 } rs_world_desc;
 
 typedef struct rs_handle_s *rs_handle;
@@ -98,8 +116,10 @@ int rs_create(const rs_world_desc *desc, rs_handle *out);
 int rs_upload(rs_handle h, uint32_t mask);
 /* Advance `steps` time steps on the device state (K steps per launch).
  * Applies commands staged with rs_stage_commands at the first step boundary.
- * contacts: always 0 in this build (no mesh / self-collision); barrier_ns:
- * 0 (barriers are on-chip).  Either pointer may be NULL. */
+ * contacts: active mesh contacts after the last step (epoch_results,
+ * _core.pyx:1133; no self-collision pairs in this build; waits for the
+ * epoch when the scene has contacts); barrier_ns: 0 (barriers are on-chip).
+ * Either pointer may be NULL. */
 int rs_run_epoch(rs_handle h, int64_t steps, int64_t *contacts, int64_t *barrier_ns);
 int rs_download(rs_handle h, uint32_t mask);
 /* rs_upload(RS_STATE) + rs_run_epoch + rs_download(RS_STATE) as one call

@@ -14,12 +14,13 @@ import numpy as np
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
                         "librodsim_b200.so")
 
-RS_ABI_VERSION = 1
+RS_ABI_VERSION = 2
 RS_OK = 0
 RS_E_INVALID = -1
 RS_E_CUDA = -2
 RS_E_UNSUPPORTED = -3
 RS_E_RING_FULL = -4
+RS_E_RUNTIME = -5
 
 RS_F64_MIRROR = 0
 RS_F32 = 1
@@ -57,6 +58,13 @@ class WorldDesc(ctypes.Structure):
         ("nbind", _i64), ("bind_a", _p), ("bind_b", _p), ("bind_mode", _p),
         ("drv_v", _p), ("drv_rot", _p),
         ("ngrab", _i64), ("g_act", _p), ("g_pt", _p), ("g_tgt", _p),
+        ("has_mesh", _i64), ("n_nodes", _i64), ("mesh_depth", _i64),
+        ("n_tris", _i64), ("n_verts", _i64),
+        ("nmin", _p), ("nmax", _p), ("nstart", _p), ("ncount", _p),
+        ("torder", _p), ("tris", _p), ("verts", _p),
+        ("cradii", _p), ("cmask", _p), ("cact", _p), ("cnorm", _p), ("cdepth", _p),
+        ("cacc_n", _p), ("cacc_t", _p),
+        ("coll_interval", _i64), ("coll_margin", _f64), ("restitution", _f64), ("mu", _f64),
     ]
 
 
@@ -181,8 +189,21 @@ def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
         "bind_mode": c(w.bind_mode, dtype=np.int64),
         "drv_v": w.driver_velocity, "drv_rot": w.driver_rotation,
         "g_act": w.grab_active, "g_pt": w.grab_point, "g_tgt": w.grab_target,
+        # contact slots are state (mutated in place, like the reference's)
+        "cradii": c(w.contact_radii), "cmask": c(w.collide_mesh_mask).view(np.uint8),
+        "cact": w.contact_active, "cnorm": w.contact_normal, "cdepth": w.contact_depth,
+        "cacc_n": w.contact_acc_n, "cacc_t": w.contact_acc_t,
     }
-    for k in ("pos", "vel", "q", "w", "drv_v", "drv_rot", "g_act", "g_pt", "g_tgt"):
+    tree = getattr(w, "tree", None)
+    if tree is not None:
+        arrays.update({
+            "nmin": c(tree.node_min, dtype=float), "nmax": c(tree.node_max, dtype=float),
+            "nstart": c(tree.node_start, dtype=np.int64),
+            "ncount": c(tree.node_count, dtype=np.int64),
+            "torder": c(tree.tri_order, dtype=np.int64),
+            "tris": c(tree.triangles, dtype=np.int64), "verts": c(tree.vertices, dtype=float)})
+    for k in ("pos", "vel", "q", "w", "drv_v", "drv_rot", "g_act", "g_pt", "g_tgt",
+              "cact", "cnorm", "cdepth", "cacc_n", "cacc_t"):
         a = arrays[k]
         if not (a.flags.c_contiguous and a.flags.writeable):
             raise ValueError(f"world array {k} must be C-contiguous and writeable")
@@ -203,6 +224,16 @@ def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
         setattr(d, name, _ptr(arr))
     d.nbind = arrays["bind_a"].shape[0]
     d.ngrab = arrays["g_act"].shape[0]
+    if tree is not None:
+        d.has_mesh = 1
+        d.n_nodes = arrays["nmin"].shape[0]
+        d.mesh_depth = int(tree.max_depth)
+        d.n_tris = arrays["tris"].shape[0]
+        d.n_verts = arrays["verts"].shape[0]
+    d.coll_interval = int(w.collision_interval)
+    d.coll_margin = float(w.collision_margin)
+    d.restitution = float(w.solver.restitution)
+    d.mu = float(w.solver.mu)
     return d, arrays
 
 

@@ -113,6 +113,17 @@ struct StepArgs {
     int32_t ntasks;                                // stream tier: tasks for gridDim CTAs
     Real dt, beta, gx, gy, gz;
     UniConsts<Real> u;                             // UNI == 2 launches
+    // mesh contacts (_core.pyx:509-662, 730-741, 906-947); contacts_on == 0:
+    // no contact slot is ever set, the machinery (and its barrier) is off
+    int32_t contacts_on, has_mesh, n_nodes, coll_interval;
+    const Real *nmin, *nmax, *verts;               // tree boxes (nodes,3), vertices (V,3)
+    const int32_t *nstart, *ncount, *torder, *tris;
+    const Real *cradii;                            // (P) contact radius
+    const uint8_t *cmask;                          // (P) collides with the mesh
+    uint8_t *cact;                                 // (P) contact slots (state)
+    Real *cnorm, *cdepth, *cacc_n, *cacc_t;        // (P,3) (P) (P) (P)
+    unsigned long long *contacts;                  // active contacts after the last step
+    Real coll_margin, restitution, mu;
 };
 
 constexpr int PROF_SLOTS = 64;

@@ -136,6 +136,12 @@ struct rs_handle_s {
     DevBuf pos, vel, q, w;
     DevBuf rest, ustar, inert, ks, kp, gt, gr, kb, mass, invm, fext, drv_v, drv_rot;
     DevBuf pflags, pt_elem, tasks, binds, drvs, grabs;
+    // mesh contacts: tree + mesh (static), contact slots (state)
+    DevBuf nmin, nmax, verts, nstart, ncount, torder, tris, cradii, cmask;
+    DevBuf cact, cnorm, cdepth, cacc_n, cacc_t;
+    int contacts_on = 0;                    // any contact machinery needed
+    unsigned long long* d_contacts = nullptr;
+    unsigned long long* h_contacts = nullptr;   // pinned
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;   // pinned
     unsigned long long* d_prof = nullptr;  // RSB_DEBUG bit 1: per-phase cycles (CTA 0)
@@ -234,6 +240,27 @@ int get_real(rs_handle h, const DevBuf& b, double* dst, size_t count) {
         const float* s = static_cast<const float*>(h->stage);
         for (size_t i = 0; i < count; ++i) dst[i] = double(s[i]);
     }
+    return RS_OK;
+}
+
+// host int64 array -> device int32 (mesh indices; validated < 2^31)
+int put_i32(rs_handle h, DevBuf& b, const int64_t* src, size_t count) {
+    std::vector<int32_t> v(count);
+    for (size_t i = 0; i < count; ++i) {
+        if (src[i] < INT32_MIN || src[i] > INT32_MAX) return fail(RS_E_INVALID, "mesh index out of int32 range");
+        v[i] = int32_t(src[i]);
+    }
+    int rc = dev_alloc(b, std::max<size_t>(count, 1) * sizeof(int32_t));
+    if (rc) return rc;
+    if (count) CK(cudaMemcpyAsync(b.p, v.data(), count * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return RS_OK;
+}
+
+int put_u8(rs_handle h, DevBuf& b, const uint8_t* src, size_t count) {
+    int rc = dev_alloc(b, std::max<size_t>(count, 1));
+    if (rc) return rc;
+    if (count) CK(cudaMemcpyAsync(b.p, src, count, cudaMemcpyHostToDevice, h->st));
     return RS_OK;
 }
 
@@ -754,6 +781,37 @@ int upload_static(rs_handle h) {
     (void)R;
     if ((rc = put_vec(h, h->pflags, pflags))) return rc;
     if ((rc = put_vec(h, h->pt_elem, pt_elem))) return rc;
+    if (d.has_mesh) {   // make_context's tree binding (_core.pyx:301-315)
+        if (d.mesh_depth + 1 > CONTACT_STACK)
+            return fail(RS_E_RUNTIME, "tree deeper than the traversal stack capacity");
+        if (d.n_nodes < 1 || d.n_tris < 1 || d.n_verts < 1) return fail(RS_E_INVALID, "empty mesh");
+        for (int64_t i = 0; i < 3 * d.n_tris; ++i)
+            if (d.tris[i] < 0 || d.tris[i] >= d.n_verts) return fail(RS_E_INVALID, "triangle vertex out of range");
+        for (int64_t i = 0; i < d.n_nodes; ++i)
+            if (d.ncount[i] > 0 && (d.nstart[i] < 0 || d.nstart[i] + d.ncount[i] > d.n_tris))
+                return fail(RS_E_INVALID, "tree leaf range out of bounds");
+        for (int64_t i = 0; i < d.n_tris; ++i)
+            if (d.torder[i] < 0 || d.torder[i] >= d.n_tris) return fail(RS_E_INVALID, "tree order out of range");
+        if ((rc = put_real(h, h->nmin, d.nmin, 3 * size_t(d.n_nodes)))) return rc;
+        if ((rc = put_real(h, h->nmax, d.nmax, 3 * size_t(d.n_nodes)))) return rc;
+        if ((rc = put_real(h, h->verts, d.verts, 3 * size_t(d.n_verts)))) return rc;
+        if ((rc = put_i32(h, h->nstart, d.nstart, size_t(d.n_nodes)))) return rc;
+        if ((rc = put_i32(h, h->ncount, d.ncount, size_t(d.n_nodes)))) return rc;
+        if ((rc = put_i32(h, h->torder, d.torder, size_t(d.n_tris)))) return rc;
+        if ((rc = put_i32(h, h->tris, d.tris, 3 * size_t(d.n_tris)))) return rc;
+    }
+    if (d.coll_interval < 1) return fail(RS_E_INVALID, "collision_interval must be >= 1");
+    // contact slots: only a mesh, or slots set by hand, make the contact
+    // machinery do anything (every step resets the accumulators and, on
+    // detection steps, the slots, _core.pyx:730-741).  Hand-set slots in a
+    // world without a mesh are seen at bind time / the next RS_STATIC upload.
+    bool on = d.has_mesh != 0;
+    for (size_t i = 0; i < P && !on; ++i)
+        on = d.cact[i] != 0 || d.cacc_n[i] != 0.0 || d.cacc_t[i] != 0.0 || std::signbit(d.cacc_n[i]) ||
+             std::signbit(d.cacc_t[i]);
+    h->contacts_on = on;
+    if ((rc = put_real(h, h->cradii, d.cradii, P))) return rc;
+    if ((rc = put_u8(h, h->cmask, d.cmask, P))) return rc;
     if ((rc = put_vec(h, h->binds, h->h_binds))) return rc;
     if ((rc = put_vec(h, h->drvs, h->h_drvs))) return rc;
     return build_grabs(h);
@@ -786,11 +844,18 @@ int upload_control(rs_handle h) {
 
 int upload_state(rs_handle h) {
     const rs_world_desc& d = h->d;
-    int rc = put_real(h, h->pos, d.pos, 3 * size_t(d.P));
+    const size_t P = size_t(d.P);
+    int rc = put_real(h, h->pos, d.pos, 3 * P);
     if (rc) return rc;
-    if ((rc = put_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
+    if ((rc = put_real(h, h->vel, d.vel, 3 * P))) return rc;
     if ((rc = put_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
-    return put_real(h, h->w, d.w, 3 * size_t(d.E));
+    if ((rc = put_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+    if (!h->contacts_on) return RS_OK;
+    if ((rc = put_u8(h, h->cact, d.cact, P))) return rc;
+    if ((rc = put_real(h, h->cnorm, d.cnorm, 3 * P))) return rc;
+    if ((rc = put_real(h, h->cdepth, d.cdepth, P))) return rc;
+    if ((rc = put_real(h, h->cacc_n, d.cacc_n, P))) return rc;
+    return put_real(h, h->cacc_t, d.cacc_t, P);
 }
 
 // Apply staged commands at the step boundary (ph_boundary, _core.pyx:477-506).
@@ -879,6 +944,28 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
             a.u.rI[k] = Real(1.0) / a.u.I[k];
         }
     }
+    a.contacts_on = h->contacts_on;
+    a.has_mesh = int32_t(h->d.has_mesh != 0);
+    a.n_nodes = int32_t(h->d.n_nodes);
+    a.coll_interval = int32_t(h->d.coll_interval);
+    a.nmin = static_cast<const Real*>(h->nmin.p);
+    a.nmax = static_cast<const Real*>(h->nmax.p);
+    a.verts = static_cast<const Real*>(h->verts.p);
+    a.nstart = static_cast<const int32_t*>(h->nstart.p);
+    a.ncount = static_cast<const int32_t*>(h->ncount.p);
+    a.torder = static_cast<const int32_t*>(h->torder.p);
+    a.tris = static_cast<const int32_t*>(h->tris.p);
+    a.cradii = static_cast<const Real*>(h->cradii.p);
+    a.cmask = static_cast<const uint8_t*>(h->cmask.p);
+    a.cact = static_cast<uint8_t*>(h->cact.p);
+    a.cnorm = static_cast<Real*>(h->cnorm.p);
+    a.cdepth = static_cast<Real*>(h->cdepth.p);
+    a.cacc_n = static_cast<Real*>(h->cacc_n.p);
+    a.cacc_t = static_cast<Real*>(h->cacc_t.p);
+    a.contacts = h->d_contacts;
+    a.coll_margin = Real(h->d.coll_margin);
+    a.restitution = Real(h->d.restitution);
+    a.mu = Real(h->d.mu);
     a.dt = Real(h->d.dt);
     a.beta = Real(h->d.beta);
     a.gx = Real(h->d.gx);
@@ -948,7 +1035,15 @@ int epoch_epilogue(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barri
     h->step += steps;
     h->snap_seq += 2 * steps;
     h->snap_step = h->step;
-    if (contacts) *contacts = 0;
+    if (contacts) {
+        *contacts = 0;
+        if (h->contacts_on) {   // epoch_results: active contacts after the last step
+            CK(cudaMemcpyAsync(h->h_contacts, h->d_contacts, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               h->st));
+            CK(cudaStreamSynchronize(h->st));
+            *contacts = int64_t(*h->h_contacts);
+        }
+    }
     if (barrier_ns) *barrier_ns = 0;
     return RS_OK;
 }
@@ -1051,7 +1146,9 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
         cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess ||
         cudaEventCreate(&h->tm0) != cudaSuccess || cudaEventCreate(&h->tm1) != cudaSuccess ||
         cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMallocHost(&h->h_err, sizeof(unsigned long long)) != cudaSuccess)
+        cudaMallocHost(&h->h_err, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&h->d_contacts, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&h->h_contacts, sizeof(unsigned long long)) != cudaSuccess)
         return bail(fail(RS_E_CUDA, "CUDA resource creation failed"));
     *h->h_err = 0;
     if (cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess)
@@ -1102,6 +1199,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
     int64_t done = 0;
     while (done < steps) {
         const int k = int(std::min<int64_t>(steps - done, kMaxStepsPerLaunch));
+        if (h->contacts_on) CK(cudaMemsetAsync(h->d_contacts, 0, sizeof(unsigned long long), h->st));
         for (const Group& g : h->groups) {
             int rc = launch_group(h, g, h->step + done, k);
             if (rc) return rc;
@@ -1136,6 +1234,14 @@ int rs_download(rs_handle h, uint32_t mask) {
         if ((rc = get_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
         if ((rc = get_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
         if ((rc = get_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+        if (h->contacts_on) {
+            const size_t P = size_t(d.P);
+            CK(cudaMemcpyAsync(d.cact, h->cact.p, P, cudaMemcpyDeviceToHost, h->st));
+            if ((rc = get_real(h, h->cnorm, d.cnorm, 3 * P))) return rc;
+            if ((rc = get_real(h, h->cdepth, d.cdepth, P))) return rc;
+            if ((rc = get_real(h, h->cacc_n, d.cacc_n, P))) return rc;
+            if ((rc = get_real(h, h->cacc_t, d.cacc_t, P))) return rc;
+        }
     }
     return rs_synchronize(h);
 }
@@ -1144,7 +1250,8 @@ int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* ba
     if (!h) return fail(RS_E_INVALID, "null handle");
     if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
     CK(cudaSetDevice(h->d.device));
-    const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 &&
+    const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 && !h->contacts_on &&
+                           !h->d.has_mesh &&
                            (h->groups[0].tier == TIER_CTA || h->groups[0].tier == TIER_STREAM) &&
                            h->groups[0].ncta >= 2 && steps <= kMaxStepsPerLaunch;
     if (!pipelined) {
@@ -1212,7 +1319,9 @@ void rs_destroy(rs_handle h) {
     if (h->st) cudaStreamSynchronize(h->st);
     for (DevBuf* b : {&h->pos, &h->vel, &h->q, &h->w, &h->rest, &h->ustar, &h->inert, &h->ks, &h->kp, &h->gt,
                       &h->gr, &h->kb, &h->mass, &h->invm, &h->fext, &h->drv_v, &h->drv_rot, &h->pflags,
-                      &h->pt_elem, &h->tasks, &h->binds, &h->drvs, &h->grabs})
+                      &h->pt_elem, &h->tasks, &h->binds, &h->drvs, &h->grabs, &h->nmin, &h->nmax, &h->verts,
+                      &h->nstart, &h->ncount, &h->torder, &h->tris, &h->cradii, &h->cmask, &h->cact, &h->cnorm,
+                      &h->cdepth, &h->cacc_n, &h->cacc_t})
         if (b->p) cudaFree(b->p);
     for (Group& g : h->groups) {
         if (g.d_flags) cudaFree(g.d_flags);
@@ -1234,6 +1343,8 @@ void rs_destroy(rs_handle h) {
     }
     if (h->d_err) cudaFree(h->d_err);
     if (h->h_err) cudaFreeHost(h->h_err);
+    if (h->d_contacts) cudaFree(h->d_contacts);
+    if (h->h_contacts) cudaFreeHost(h->h_contacts);
     if (h->stage) cudaFreeHost(h->stage);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);

@@ -40,11 +40,13 @@ _STATIC_ATTRS = ("rest_lengths", "intrinsic_strains", "masses", "inv_masses",
                  "gamma_t", "gamma_r", "extensible", "bend_k", "point_locked",
                  "frame_locked", "junction_valid", "elem_point", "elem_parity",
                  "driven_point", "driven_frame", "bind_a", "bind_b",
-                 "bind_mode")
+                 "bind_mode", "contact_radii", "collide_mesh_mask")
 _BOUND_ATTRS = _STATIC_ATTRS + ("positions", "velocities", "frames",
                                 "angular_velocities", "driver_velocity",
                                 "driver_rotation", "grab_active",
-                                "grab_point", "grab_target")
+                                "grab_point", "grab_target", "contact_active",
+                                "contact_normal", "contact_depth", "contact_acc_n",
+                                "contact_acc_t")
 
 
 @dataclass
@@ -162,10 +164,6 @@ class Engine:
                  device=0, force_tier=-1, force_ctas=0, force_variant=-1):
         if backend not in ("serial", "parallel"):
             raise ValueError("backend must be 'serial' or 'parallel'")
-        if world.tree is not None:
-            raise NotImplementedError(
-                "mesh contacts are not in this build's hot-path scope "
-                "(SURVEY.md §8(f) next #1)")
         if world.self_collision_enabled:
             raise NotImplementedError(
                 "self-collision is not in this build's hot-path scope "
@@ -200,17 +198,25 @@ class Engine:
                                      force_tier=ft, force_ctas=fc,
                                      force_variant=fv)
         self._bound = {a: getattr(self.world, a) for a in _BOUND_ATTRS}
+        # the mesh and the collision scalars are bound too (make_context)
+        self._bound_scene = self._scene_key()
         self._static_version = self.world.static_version
         self._small = self.world.num_points <= SMALL_WORLD_POINTS
         self._static_copy = ({a: np.array(getattr(self.world, a), copy=True)
                               for a in _STATIC_ATTRS} if self._small else None)
+
+    def _scene_key(self):
+        w = self.world
+        return (id(w.tree), w.collision_interval, w.collision_margin,
+                w.solver.restitution, w.solver.mu)
 
     def _push(self, state=True):
         """Host -> device before an epoch.  Returns False when the World had
         to be re-bound (everything, state included, is then uploaded);
         state=False leaves the state to rs_run_epoch_host."""
         w = self.world
-        if any(getattr(w, a) is not arr for a, arr in self._bound.items()):
+        if (any(getattr(w, a) is not arr for a, arr in self._bound.items())
+                or self._scene_key() != self._bound_scene):
             # an array attribute was replaced: re-bind (re-plans and uploads)
             self._bind()
             return False

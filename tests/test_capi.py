@@ -139,10 +139,24 @@ def test_engine_fails_loudly_without_a_device():
 
 
 def test_engine_rejects_out_of_scope_scenes():
+    from paper_2509_04277_b200.constraints import SolverConfig
     from paper_2509_04277_b200.engine import Engine
-    w = wl.cantilever()
-    w.set_mesh(object())
-    with pytest.raises(NotImplementedError, match="mesh"):
+    w = World(dt=1e-4, solver=SolverConfig(), self_collision=object())
+    w.add_rod(st.init_rod(10, 0.1), st.RodParams())
+    w.finalize()
+    with pytest.raises(NotImplementedError, match="self-collision"):
         Engine(w)
     with pytest.raises(ValueError):
         Engine(wl.cantilever(), backend="gpu")
+
+
+def test_desc_binds_the_mesh_tree():
+    from paper_2509_04277_b200 import _lib
+    w = wl.insertion(points=20, length=0.05, tube={"rings": 12, "segments": 8})
+    d, keep = _lib.build_desc(w)
+    assert d.has_mesh == 1 and d.n_tris == w.tree.triangles.shape[0]
+    assert d.n_nodes == w.tree.node_min.shape[0] and d.mesh_depth == w.tree.max_depth
+    assert d.coll_interval == 4 and d.coll_margin == 5e-4
+    assert keep["tris"].dtype == np.int64 and keep["cact"] is w.contact_active
+    p = _lib.plan_dry(w)
+    assert p["groups"][0]["tier"] == "cta"

@@ -18,7 +18,8 @@ from paper_2509_04277_b200.engine import Engine  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("case", choices=["hair", "pair", "sweep", "cantilever", "extensible"])
+    ap.add_argument("case", choices=["hair", "pair", "sweep", "cantilever", "extensible",
+                                     "insertion", "floor_drop"])
     ap.add_argument("--rods", type=int, default=65536)
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--k", type=int, default=1)
