@@ -56,6 +56,11 @@ class RoWorld(ctypes.Structure):
         ("cacc_n", _p), ("cacc_t", _p),
         ("coll_interval", _i64), ("coll_margin", _f64), ("restitution", _f64), ("mu", _f64),
         ("contacts", _i64),
+        ("has_self", _i64), ("n_groups", _i64), ("excl", _i64), ("pair_cap", _i64),
+        ("grp_rod", _p), ("grp_gi", _p), ("grp_s", _p), ("grp_e", _p), ("grp_c", _p),
+        ("touch", _f64), ("broad", _f64),
+        ("pair_a", _p), ("pair_b", _p), ("pair_md", _p), ("pair_acc", _p),
+        ("pairs", _i64),
     ]
 
 
@@ -84,8 +89,6 @@ class OracleStepper:
     """Steps a World's arrays in place with the C restatement."""
 
     def __init__(self, world):
-        if getattr(world, "self_collision_enabled", False):
-            raise NotImplementedError("oracle does not cover self-collision")
         self.lib = load_oracle()
         self.world = w = world
         c = np.ascontiguousarray
@@ -120,6 +123,14 @@ class OracleStepper:
             "cact": w.contact_active, "cnorm": w.contact_normal, "cdepth": w.contact_depth,
             "cacc_n": w.contact_acc_n, "cacc_t": w.contact_acc_t,
         }
+        cfg = w.self_collision if getattr(w, "self_collision_enabled", False) else None
+        if cfg is not None:
+            from paper_2509_04277_b200.selfcollide import world_groups
+            g_rod, g_gi, g_s, g_e = world_groups(w, cfg.group_size)
+            self.keep.update({"grp_rod": g_rod, "grp_gi": g_gi, "grp_s": g_s, "grp_e": g_e,
+                              "grp_c": np.zeros((g_rod.shape[0], 3)),
+                              "pair_a": w.pair_a, "pair_b": w.pair_b,
+                              "pair_md": w.pair_min_dist, "pair_acc": w.pair_acc})
         tree = getattr(w, "tree", None)
         if tree is not None:
             if tree.max_depth + 1 > 32:
@@ -148,6 +159,13 @@ class OracleStepper:
         s.coll_margin = float(w.collision_margin)
         s.restitution = float(w.solver.restitution)
         s.mu = float(w.solver.mu)
+        if cfg is not None:
+            s.has_self = 1
+            s.n_groups = self.keep["grp_rod"].shape[0]
+            s.excl = int(cfg.neighbor_exclusion)
+            s.touch = 2.0 * cfg.point_radius
+            s.broad = 2.0 * cfg.sphere_radius
+            s.pair_cap = w.pair_a.shape[0]
         self.s = s
         self.lib.ro_prepare(ctypes.byref(s))
 
@@ -161,8 +179,9 @@ class OracleStepper:
 
     @property
     def contacts(self):
-        """Active mesh contacts after the last step (step_serial's return)."""
-        return int(self.s.contacts)
+        """Active mesh contacts + self-collision pairs after the last step
+        (step_serial's return, _core.pyx:1080)."""
+        return int(self.s.contacts) + int(self.s.pairs)
 
 
 # ---- the reference's own compiled core ---------------------------------------

@@ -335,6 +335,57 @@ void ro_scatter(ro_world *w)
         scatter_element(w, e);
 }
 
+/* ---- self-collision broad phase (_core.pyx:665-708) ---------------------- */
+
+void ro_selfpairs(ro_world *w)
+{
+    if (!w->has_self)
+        return;
+    if (w->step % w->coll_interval != 0) {   /* reuse the set, reset accumulators */
+        for (int64_t k = 0; k < w->pairs; ++k) w->pair_acc[k] = 0.0;
+        return;
+    }
+    for (int64_t g = 0; g < w->n_groups; ++g) {
+        double *c = w->grp_c + 3 * g;
+        c[0] = 0.0;
+        c[1] = 0.0;
+        c[2] = 0.0;
+        for (int64_t i = w->grp_s[g]; i < w->grp_e[g]; ++i)
+            for (int k = 0; k < 3; ++k) c[k] += w->pos[3 * i + k];
+        const double inv = 1.0 / (double)(w->grp_e[g] - w->grp_s[g]);
+        for (int k = 0; k < 3; ++k) c[k] *= inv;
+    }
+    int64_t cnt = 0;
+    for (int64_t a = 0; a < w->n_groups; ++a) {
+        for (int64_t b = a + 1; b < w->n_groups; ++b) {
+            if (w->grp_rod[a] == w->grp_rod[b]) {
+                const int64_t g = w->grp_gi[a] - w->grp_gi[b];
+                if (-w->excl <= g && g <= w->excl)
+                    continue;
+            }
+            const double *ca = w->grp_c + 3 * a, *cb = w->grp_c + 3 * b;
+            double dx = cb[0] - ca[0], dy = cb[1] - ca[1], dz = cb[2] - ca[2];
+            if (dx * dx + dy * dy + dz * dz >= w->broad * w->broad)
+                continue;
+            for (int64_t i = w->grp_s[a]; i < w->grp_e[a]; ++i) {
+                for (int64_t j = w->grp_s[b]; j < w->grp_e[b]; ++j) {
+                    dx = w->pos[3 * j] - w->pos[3 * i];
+                    dy = w->pos[3 * j + 1] - w->pos[3 * i + 1];
+                    dz = w->pos[3 * j + 2] - w->pos[3 * i + 2];
+                    if (dx * dx + dy * dy + dz * dz < w->touch * w->touch && cnt < w->pair_cap) {
+                        w->pair_a[cnt] = i;
+                        w->pair_b[cnt] = j;
+                        w->pair_md[cnt] = w->touch;
+                        w->pair_acc[cnt] = 0.0;
+                        cnt += 1;
+                    }
+                }
+            }
+        }
+    }
+    w->pairs = cnt;
+}
+
 /* ---- contact impulses with accumulator and box friction (_core.pyx:906-947) */
 
 void ro_contacts(ro_world *w)
@@ -475,6 +526,34 @@ void ro_distance(ro_world *w, int64_t parity)
 
 void ro_central(ro_world *w)
 {
+    /* self-collision pairs, in list order (_core.pyx:956-980) */
+    for (int64_t k = 0; k < w->pairs; ++k) {
+        const int64_t a = w->pair_a[k], b = w->pair_b[k];
+        double d[3], n[3];
+        for (int i = 0; i < 3; ++i) d[i] = w->pos[3 * b + i] - w->pos[3 * a + i];
+        const double dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        const double wsum = w->invm[a] + w->invm[b];
+        if (dist == 0.0 || wsum == 0.0)
+            continue;
+        double vrel = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            n[i] = d[i] / dist;
+            vrel += (w->vel[3 * b + i] - w->vel[3 * a + i]) * n[i];
+        }
+        double depth = w->pair_md[k] - dist;
+        if (depth < 0.0)
+            depth = 0.0;
+        const double raw = (-vrel + w->beta * depth / w->dt) / wsum;
+        double new_acc = w->pair_acc[k] + raw;
+        if (new_acc < 0.0)
+            new_acc = 0.0;
+        const double lam = new_acc - w->pair_acc[k];
+        w->pair_acc[k] = new_acc;
+        for (int i = 0; i < 3; ++i) {
+            w->vel[3 * a + i] -= w->invm[a] * lam * n[i];
+            w->vel[3 * b + i] += w->invm[b] * lam * n[i];
+        }
+    }
     for (int64_t k = 0; k < w->nbind; ++k) {
         const int64_t a = w->bind_a[k], b = w->bind_b[k];
         const double wa = w->bind_mode[k] == 0 ? 0.0 : w->invm[a];
@@ -540,7 +619,10 @@ void ro_integrate(ro_world *w)
 void ro_run(ro_world *w, int64_t steps)
 {
     for (int64_t s = 0; s < steps; ++s) {
+        if (w->step % (w->coll_interval > 0 ? w->coll_interval : 1) == 0)
+            w->pairs = 0;                   /* ph_boundary (_core.pyx:504-505) */
         ro_scatter(w);
+        ro_selfpairs(w);
         ro_gather(w);
         for (int64_t it = 0; it < w->iters; ++it) {
             ro_distance(w, 0);

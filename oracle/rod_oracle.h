@@ -11,7 +11,7 @@
  * per-element material arrays, per-point/per-frame lock flags, drivers,
  * bindings and grab anchors.  The stepping semantics follow the reference's
  * compiled serial step (_core.pyx:1058-1080): elastic forces, constraints,
- * bindings, grabs and mesh contacts; no self-collision.
+ * bindings, grabs, mesh contacts and self-collision pairs.
  */
 #ifndef ROD_ORACLE_H
 #define ROD_ORACLE_H
@@ -68,6 +68,14 @@ typedef struct ro_world {
     int64_t coll_interval;
     double coll_margin, restitution, mu;
     int64_t contacts;            /* active contacts after the last step */
+    /* self-collision (_core.pyx:665-708, 956-980); has_self 0: none */
+    int64_t has_self, n_groups, excl, pair_cap;
+    const int64_t *grp_rod, *grp_gi, *grp_s, *grp_e;   /* (G) group table */
+    double *grp_c;                                     /* (G,3) scratch */
+    double touch, broad;
+    int64_t *pair_a, *pair_b;    /* (pair_cap) world.pair_a / pair_b */
+    double *pair_md, *pair_acc;  /* world.pair_min_dist / pair_acc */
+    int64_t pairs;               /* CNT_PAIRS: pairs in the current set */
 } ro_world;
 
 /* Build pt_elo / pt_ehi from elem_point (make_context, _core.pyx:264-272). */
@@ -80,6 +88,7 @@ void ro_gather(ro_world *w);
 void ro_distance(ro_world *w, int64_t parity);
 void ro_central(ro_world *w);
 void ro_contacts(ro_world *w);
+void ro_selfpairs(ro_world *w);
 void ro_integrate(ro_world *w);
 
 #ifdef __cplusplus

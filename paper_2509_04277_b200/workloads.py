@@ -8,6 +8,8 @@ cfg4 `sweep`       single inextensible rod of N elements, l = 2 mm
 cfg5 `hair`        R rods x 128 elements, roots clamped, random directions
 `insertion`        guidewire pushed into a curved tube mesh (mesh contacts)
 `floor_drop`       rod dropped onto a floor mesh (contacts + friction)
+`knot`             two threads knotted by a recorded grab session (self-collision)
+`crossing`         two rods pushed across each other (self-collision pairs)
 
 All use the scenario material defaults (scenarios.py:30-32): r = 1 mm,
 E_s = 1e7, E_b = G = 1e6, rho = 0.05 kg/m, K_p = 1, gamma_t = 2e-4,
@@ -146,5 +148,50 @@ def floor_drop(points=33, length=0.2, height=0.02, restitution=0.0, mu=0.3):
     return w
 
 
+THREAD = dict(MATERIAL, bend_modulus=5e3, shear_modulus=5e3,
+              damping_translational=2e-3, damping_rotational=1e-7)
+
+
+def knot():
+    """The reference's knot_replay scene (scenarios.py:79-101 through
+    scene.build_world, scene.py:262-319): two soft 48-point threads 2 cm
+    apart, roots clamped, no gravity, I = 15, beta = 0.5, self-collision
+    (groups of 4, 2 cm spheres, 2-group exclusion, 1 mm points).  Driven by
+    the recorded grab session tests/golden/knot_session.ndjson."""
+    from .selfcollide import SelfCollisionConfig
+    w = World(dt=1e-4, gravity=(0.0, 0.0, 0.0),
+              solver=SolverConfig(iterations=15, position_bias=0.5),
+              self_collision=SelfCollisionConfig(group_size=4, sphere_radius=0.02,
+                                                 neighbor_exclusion=2, point_radius=1e-3))
+    for z in (0.0, 0.02):
+        w.add_rod(st.init_rod(48, 0.24, axis=(1.0, 0.0, 0.0), origin=(-0.12, 0.0, z)),
+                  st.RodParams(**THREAD))
+    w.finalize()
+    w.collision_interval = 1
+    w.collision_margin = 0.0
+    for r in (0, 1):
+        w.clamp_point(r, 0)
+    return w
+
+
+def crossing(points=24, interval=1):
+    """Two rods crossing 1.5 mm apart and pushed together: self-collision
+    pairs between rods (quick fixture for the pair phase)."""
+    from .selfcollide import SelfCollisionConfig
+    w = World(dt=1e-4, gravity=(0.0, 0.0, 0.0), solver=SolverConfig(iterations=10),
+              self_collision=SelfCollisionConfig(group_size=4, sphere_radius=0.01,
+                                                 neighbor_exclusion=2, point_radius=1e-3))
+    w.add_rod(st.init_rod(points, 0.05, axis=(1.0, 0.0, 0.0), origin=(-0.025, 0.0, 0.0)),
+              st.RodParams(**THREAD))
+    w.add_rod(st.init_rod(points, 0.05, axis=(0.0, 1.0, 0.0), origin=(0.0, -0.025, 0.0015)),
+              st.RodParams(**THREAD))
+    w.finalize()
+    w.collision_interval = interval
+    o = w.rod_infos[1].point_offset
+    w.velocities[o:o + points] = (0.0, 0.0, -0.2)
+    return w
+
+
 BUILDERS = {"cantilever": cantilever, "extensible": extensible, "pair": pair,
-            "sweep": sweep, "hair": hair, "insertion": insertion, "floor_drop": floor_drop}
+            "sweep": sweep, "hair": hair, "insertion": insertion, "floor_drop": floor_drop,
+            "knot": knot, "crossing": crossing}

@@ -137,5 +137,26 @@ def main():
               f"{os.path.getsize(path) / 1e3:.0f} kB")
 
 
+def copy_knot_assets():
+    """The reference's own knot-replay golden data (scenarios.py:86-101,
+    test_acceptance.py:455-490): the recorded command session and the
+    position checksum after 16000 steps, copied verbatim as fixtures."""
+    import json
+    import shutil
+    src = os.path.join(REF_SRC, "rodsim", "assets")
+    shutil.copyfile(os.path.join(src, "knot_session.ndjson"),
+                    os.path.join(HERE, "knot_session.ndjson"))
+    with open(os.path.join(src, "knot_checksum.json")) as fh:
+        rec = json.load(fh)
+    with open(os.path.join(HERE, "knot_checksum.json"), "w") as fh:
+        json.dump(rec, fh, indent=2)
+        fh.write("\n")
+    print("knot assets:", rec)
+
+
 if __name__ == "__main__":
-    main()
+    if "--knot" in sys.argv:
+        copy_knot_assets()
+    else:
+        main()
+        copy_knot_assets()
