@@ -108,6 +108,16 @@ typedef struct rs_world_desc {
     int64_t coll_interval;            /* world.collision_interval */
     double coll_margin;               /* world.collision_margin */
     double restitution, mu;           /* solver.restitution, solver.mu */
+    /* self-collision (ABI 2; has_self 0: none): the point-group table as
+     * make_context builds it (_core.pyx:316-345) and the world's pair
+     * buffers (world.py:164-168, state).  All rods must fit one CTA-tier
+     * segment (<= 513 points): the pairs couple arbitrary points and are
+     * applied in list order. */
+    int64_t has_self, n_groups, excl, pair_cap;
+    const int64_t *grp_rod, *grp_gi, *grp_s, *grp_e;   /* (n_groups) */
+    double touch, broad;              /* 2 point_radius, 2 sphere_radius */
+    int64_t *pair_a, *pair_b;         /* (pair_cap) */
+    double *pair_md, *pair_acc;       /* (pair_cap) */
 } rs_world_desc;
 
 typedef struct rs_handle_s *rs_handle;
@@ -116,9 +126,9 @@ int rs_create(const rs_world_desc *desc, rs_handle *out);
 int rs_upload(rs_handle h, uint32_t mask);
 /* Advance `steps` time steps on the device state (K steps per launch).
  * Applies commands staged with rs_stage_commands at the first step boundary.
- * contacts: active mesh contacts after the last step (epoch_results,
- * _core.pyx:1133; no self-collision pairs in this build; waits for the
- * epoch when the scene has contacts); barrier_ns: 0 (barriers are on-chip).
+ * contacts: active mesh contacts + self-collision pairs after the last
+ * step (epoch_results, _core.pyx:1133; waits for the epoch when the scene
+ * has contacts); barrier_ns: 0 (barriers are on-chip).
  * Either pointer may be NULL. */
 int rs_run_epoch(rs_handle h, int64_t steps, int64_t *contacts, int64_t *barrier_ns);
 int rs_download(rs_handle h, uint32_t mask);

@@ -65,6 +65,10 @@ class WorldDesc(ctypes.Structure):
         ("cradii", _p), ("cmask", _p), ("cact", _p), ("cnorm", _p), ("cdepth", _p),
         ("cacc_n", _p), ("cacc_t", _p),
         ("coll_interval", _i64), ("coll_margin", _f64), ("restitution", _f64), ("mu", _f64),
+        ("has_self", _i64), ("n_groups", _i64), ("excl", _i64), ("pair_cap", _i64),
+        ("grp_rod", _p), ("grp_gi", _p), ("grp_s", _p), ("grp_e", _p),
+        ("touch", _f64), ("broad", _f64),
+        ("pair_a", _p), ("pair_b", _p), ("pair_md", _p), ("pair_acc", _p),
     ]
 
 
@@ -194,6 +198,13 @@ def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
         "cact": w.contact_active, "cnorm": w.contact_normal, "cdepth": w.contact_depth,
         "cacc_n": w.contact_acc_n, "cacc_t": w.contact_acc_t,
     }
+    cfg = w.self_collision if getattr(w, "self_collision_enabled", False) else None
+    if cfg is not None:
+        from .selfcollide import world_groups
+        g_rod, g_gi, g_s, g_e = world_groups(w, cfg.group_size)
+        arrays.update({"grp_rod": g_rod, "grp_gi": g_gi, "grp_s": g_s, "grp_e": g_e,
+                       "pair_a": w.pair_a, "pair_b": w.pair_b, "pair_md": w.pair_min_dist,
+                       "pair_acc": w.pair_acc})
     tree = getattr(w, "tree", None)
     if tree is not None:
         arrays.update({
@@ -234,6 +245,13 @@ def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
     d.coll_margin = float(w.collision_margin)
     d.restitution = float(w.solver.restitution)
     d.mu = float(w.solver.mu)
+    if cfg is not None:
+        d.has_self = 1
+        d.n_groups = arrays["grp_rod"].shape[0]
+        d.excl = int(cfg.neighbor_exclusion)
+        d.pair_cap = arrays["pair_a"].shape[0]
+        d.touch = 2.0 * cfg.point_radius
+        d.broad = 2.0 * cfg.sphere_radius
     return d, arrays
 
 

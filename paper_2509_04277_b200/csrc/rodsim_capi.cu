@@ -139,6 +139,9 @@ struct rs_handle_s {
     // mesh contacts: tree + mesh (static), contact slots (state)
     DevBuf nmin, nmax, verts, nstart, ncount, torder, tris, cradii, cmask;
     DevBuf cact, cnorm, cdepth, cacc_n, cacc_t;
+    // self-collision: group table (static), pair list (state), count (device)
+    DevBuf grp_rod, grp_gi, grp_s, grp_e, grp_c, pair_a, pair_b, pair_md, pair_acc;
+    int32_t* d_pairs = nullptr;             // CNT_PAIRS, persistent like the ctx counter
     int contacts_on = 0;                    // any contact machinery needed
     unsigned long long* d_contacts = nullptr;
     unsigned long long* h_contacts = nullptr;   // pinned
@@ -367,6 +370,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     // reach[r] = furthest rod that must share a segment with r
     std::vector<int> reach(R);
     std::iota(reach.begin(), reach.end(), 0);
+    if (d.has_self) reach[0] = int(R - 1);   // pairs may couple any two points
     for (int64_t k = 0; k < d.nbind; ++k) {
         const int a = int(std::min(rodA[k], rodB[k])), b = int(std::max(rodA[k], rodB[k]));
         reach[a] = std::max(reach[a], b);
@@ -398,6 +402,9 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         const int64_t np = segs[i].p1 - segs[i].p0;
         int tier = np <= cta_cap ? TIER_CTA : (np <= int64_t(kMaxCluster) * clu_cap ? TIER_CLUSTER : TIER_GRID);
         if (d.force_tier >= 0) tier = d.force_tier;
+        if (d.has_self && tier != TIER_CTA)
+            return fail(RS_E_UNSUPPORTED, "self-collision scenes must fit one CTA (%d points, have %lld)", cta_cap,
+                        (long long)np);
         if (tier == TIER_CTA && np > cta_cap)
             return fail(RS_E_INVALID, "segment of %lld points does not fit one CTA", (long long)np);
         if (tier == TIER_GRID) {
@@ -801,6 +808,17 @@ int upload_static(rs_handle h) {
         if ((rc = put_i32(h, h->tris, d.tris, 3 * size_t(d.n_tris)))) return rc;
     }
     if (d.coll_interval < 1) return fail(RS_E_INVALID, "collision_interval must be >= 1");
+    if (d.has_self) {
+        if (d.n_groups < 1 || d.pair_cap < 1) return fail(RS_E_INVALID, "self-collision needs groups and pair buffers");
+        for (int64_t g = 0; g < d.n_groups; ++g)
+            if (d.grp_s[g] < 0 || d.grp_e[g] > d.P || d.grp_s[g] >= d.grp_e[g])
+                return fail(RS_E_INVALID, "self-collision group %lld out of range", (long long)g);
+        if ((rc = put_i32(h, h->grp_rod, d.grp_rod, size_t(d.n_groups)))) return rc;
+        if ((rc = put_i32(h, h->grp_gi, d.grp_gi, size_t(d.n_groups)))) return rc;
+        if ((rc = put_i32(h, h->grp_s, d.grp_s, size_t(d.n_groups)))) return rc;
+        if ((rc = put_i32(h, h->grp_e, d.grp_e, size_t(d.n_groups)))) return rc;
+        if ((rc = dev_alloc(h->grp_c, h->rsz * 3 * size_t(d.n_groups)))) return rc;
+    }
     // contact slots: only a mesh, or slots set by hand, make the contact
     // machinery do anything (every step resets the accumulators and, on
     // detection steps, the slots, _core.pyx:730-741).  Hand-set slots in a
@@ -850,6 +868,12 @@ int upload_state(rs_handle h) {
     if ((rc = put_real(h, h->vel, d.vel, 3 * P))) return rc;
     if ((rc = put_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
     if ((rc = put_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+    if (d.has_self) {
+        if ((rc = put_i32(h, h->pair_a, d.pair_a, size_t(d.pair_cap)))) return rc;
+        if ((rc = put_i32(h, h->pair_b, d.pair_b, size_t(d.pair_cap)))) return rc;
+        if ((rc = put_real(h, h->pair_md, d.pair_md, size_t(d.pair_cap)))) return rc;
+        if ((rc = put_real(h, h->pair_acc, d.pair_acc, size_t(d.pair_cap)))) return rc;
+    }
     if (!h->contacts_on) return RS_OK;
     if ((rc = put_u8(h, h->cact, d.cact, P))) return rc;
     if ((rc = put_real(h, h->cnorm, d.cnorm, 3 * P))) return rc;
@@ -963,6 +987,22 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.cacc_n = static_cast<Real*>(h->cacc_n.p);
     a.cacc_t = static_cast<Real*>(h->cacc_t.p);
     a.contacts = h->d_contacts;
+    a.has_self = int32_t(h->d.has_self != 0);
+    a.n_groups = int32_t(h->d.n_groups);
+    a.excl = int32_t(h->d.excl);
+    a.pair_cap = int32_t(std::min<int64_t>(h->d.pair_cap, INT32_MAX));
+    a.grp_rod = static_cast<const int32_t*>(h->grp_rod.p);
+    a.grp_gi = static_cast<const int32_t*>(h->grp_gi.p);
+    a.grp_s = static_cast<const int32_t*>(h->grp_s.p);
+    a.grp_e = static_cast<const int32_t*>(h->grp_e.p);
+    a.grp_c = static_cast<Real*>(h->grp_c.p);
+    a.pair_a = static_cast<int32_t*>(h->pair_a.p);
+    a.pair_b = static_cast<int32_t*>(h->pair_b.p);
+    a.pair_md = static_cast<Real*>(h->pair_md.p);
+    a.pair_acc = static_cast<Real*>(h->pair_acc.p);
+    a.pair_count = h->d_pairs;
+    a.touch = Real(h->d.touch);
+    a.broad = Real(h->d.broad);
     a.coll_margin = Real(h->d.coll_margin);
     a.restitution = Real(h->d.restitution);
     a.mu = Real(h->d.mu);
@@ -1037,7 +1077,7 @@ int epoch_epilogue(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barri
     h->snap_step = h->step;
     if (contacts) {
         *contacts = 0;
-        if (h->contacts_on) {   // epoch_results: active contacts after the last step
+        if (h->contacts_on || h->d.has_self) {   // epoch_results: contacts + pairs after the last step
             CK(cudaMemcpyAsync(h->h_contacts, h->d_contacts, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                h->st));
             CK(cudaStreamSynchronize(h->st));
@@ -1148,6 +1188,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
         cudaMalloc(&h->d_err, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMallocHost(&h->h_err, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&h->d_contacts, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&h->d_pairs, sizeof(int32_t)) != cudaSuccess || cudaMemset(h->d_pairs, 0, sizeof(int32_t)) != cudaSuccess ||
         cudaMallocHost(&h->h_contacts, sizeof(unsigned long long)) != cudaSuccess)
         return bail(fail(RS_E_CUDA, "CUDA resource creation failed"));
     *h->h_err = 0;
@@ -1199,7 +1240,8 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
     int64_t done = 0;
     while (done < steps) {
         const int k = int(std::min<int64_t>(steps - done, kMaxStepsPerLaunch));
-        if (h->contacts_on) CK(cudaMemsetAsync(h->d_contacts, 0, sizeof(unsigned long long), h->st));
+        if (h->contacts_on || h->d.has_self)
+            CK(cudaMemsetAsync(h->d_contacts, 0, sizeof(unsigned long long), h->st));
         for (const Group& g : h->groups) {
             int rc = launch_group(h, g, h->step + done, k);
             if (rc) return rc;
@@ -1234,6 +1276,19 @@ int rs_download(rs_handle h, uint32_t mask) {
         if ((rc = get_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
         if ((rc = get_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
         if ((rc = get_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+        if (d.has_self) {
+            const size_t n = size_t(d.pair_cap);
+            std::vector<int32_t> ia(n), ib(n);
+            CK(cudaMemcpyAsync(ia.data(), h->pair_a.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaMemcpyAsync(ib.data(), h->pair_b.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+            if ((rc = get_real(h, h->pair_md, d.pair_md, n))) return rc;
+            if ((rc = get_real(h, h->pair_acc, d.pair_acc, n))) return rc;
+            CK(cudaStreamSynchronize(h->st));
+            for (size_t i = 0; i < n; ++i) {
+                d.pair_a[i] = ia[i];
+                d.pair_b[i] = ib[i];
+            }
+        }
         if (h->contacts_on) {
             const size_t P = size_t(d.P);
             CK(cudaMemcpyAsync(d.cact, h->cact.p, P, cudaMemcpyDeviceToHost, h->st));
@@ -1251,7 +1306,7 @@ int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* ba
     if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
     CK(cudaSetDevice(h->d.device));
     const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 && !h->contacts_on &&
-                           !h->d.has_mesh &&
+                           !h->d.has_mesh && !h->d.has_self &&
                            (h->groups[0].tier == TIER_CTA || h->groups[0].tier == TIER_STREAM) &&
                            h->groups[0].ncta >= 2 && steps <= kMaxStepsPerLaunch;
     if (!pipelined) {
@@ -1321,7 +1376,8 @@ void rs_destroy(rs_handle h) {
                       &h->gr, &h->kb, &h->mass, &h->invm, &h->fext, &h->drv_v, &h->drv_rot, &h->pflags,
                       &h->pt_elem, &h->tasks, &h->binds, &h->drvs, &h->grabs, &h->nmin, &h->nmax, &h->verts,
                       &h->nstart, &h->ncount, &h->torder, &h->tris, &h->cradii, &h->cmask, &h->cact, &h->cnorm,
-                      &h->cdepth, &h->cacc_n, &h->cacc_t})
+                      &h->cdepth, &h->cacc_n, &h->cacc_t, &h->grp_rod, &h->grp_gi, &h->grp_s, &h->grp_e,
+                      &h->grp_c, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc})
         if (b->p) cudaFree(b->p);
     for (Group& g : h->groups) {
         if (g.d_flags) cudaFree(g.d_flags);
@@ -1344,6 +1400,7 @@ void rs_destroy(rs_handle h) {
     if (h->d_err) cudaFree(h->d_err);
     if (h->h_err) cudaFreeHost(h->h_err);
     if (h->d_contacts) cudaFree(h->d_contacts);
+    if (h->d_pairs) cudaFree(h->d_pairs);
     if (h->h_contacts) cudaFreeHost(h->h_contacts);
     if (h->stage) cudaFreeHost(h->stage);
     if (h->ev0) cudaEventDestroy(h->ev0);

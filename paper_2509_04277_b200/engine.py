@@ -46,7 +46,8 @@ _BOUND_ATTRS = _STATIC_ATTRS + ("positions", "velocities", "frames",
                                 "driver_rotation", "grab_active",
                                 "grab_point", "grab_target", "contact_active",
                                 "contact_normal", "contact_depth", "contact_acc_n",
-                                "contact_acc_t")
+                                "contact_acc_t", "pair_a", "pair_b", "pair_min_dist",
+                                "pair_acc")
 
 
 @dataclass
@@ -164,10 +165,6 @@ class Engine:
                  device=0, force_tier=-1, force_ctas=0, force_variant=-1):
         if backend not in ("serial", "parallel"):
             raise ValueError("backend must be 'serial' or 'parallel'")
-        if world.self_collision_enabled:
-            raise NotImplementedError(
-                "self-collision is not in this build's hot-path scope "
-                "(SURVEY.md §8(f) next #2)")
         self.world = world
         self.backend = backend
         self.precision = precision
@@ -207,8 +204,8 @@ class Engine:
 
     def _scene_key(self):
         w = self.world
-        return (id(w.tree), w.collision_interval, w.collision_margin,
-                w.solver.restitution, w.solver.mu)
+        return (id(w.tree), id(w.self_collision), w.collision_interval,
+                w.collision_margin, w.solver.restitution, w.solver.mu)
 
     def _push(self, state=True):
         """Host -> device before an epoch.  Returns False when the World had

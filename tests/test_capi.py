@@ -139,15 +139,22 @@ def test_engine_fails_loudly_without_a_device():
 
 
 def test_engine_rejects_out_of_scope_scenes():
-    from paper_2509_04277_b200.constraints import SolverConfig
     from paper_2509_04277_b200.engine import Engine
-    w = World(dt=1e-4, solver=SolverConfig(), self_collision=object())
-    w.add_rod(st.init_rod(10, 0.1), st.RodParams())
-    w.finalize()
-    with pytest.raises(NotImplementedError, match="self-collision"):
-        Engine(w)
     with pytest.raises(ValueError):
         Engine(wl.cantilever(), backend="gpu")
+
+
+def test_self_collision_plan_is_one_cta():
+    g = plan(wl.knot())
+    assert len(g) == 1 and g[0]["tier"] == "cta" and g[0]["ctas"] == 1 and g[0]["points"] == 96
+    from paper_2509_04277_b200.constraints import SolverConfig
+    from paper_2509_04277_b200.selfcollide import SelfCollisionConfig
+    w = World(dt=1e-4, solver=SolverConfig(), self_collision=SelfCollisionConfig())
+    for _ in range(3):
+        w.add_rod(st.init_rod(300, 0.3), st.RodParams())
+    w.finalize()
+    with pytest.raises(NotImplementedError, match="self-collision"):
+        plan(w)
 
 
 def test_desc_binds_the_mesh_tree():
