@@ -154,9 +154,25 @@ def copy_knot_assets():
     print("knot assets:", rec)
 
 
+def copy_scenario_assets():
+    """Data files the bundled scenarios load (scenarios.py:45-101): the
+    curved-tube mesh of the insertion scenes and the knot session log,
+    copied verbatim into the package's assets directory."""
+    import shutil
+    src = os.path.join(REF_SRC, "rodsim", "assets")
+    dst = os.path.join(ROOT, "paper_2509_04277_b200", "assets")
+    os.makedirs(dst, exist_ok=True)
+    for name in ("curved_tube.obj", "knot_session.ndjson"):
+        shutil.copyfile(os.path.join(src, name), os.path.join(dst, name))
+    print("scenario assets ->", dst)
+
+
 if __name__ == "__main__":
     if "--knot" in sys.argv:
         copy_knot_assets()
+    elif "--assets" in sys.argv:
+        copy_scenario_assets()
     else:
         main()
         copy_knot_assets()
+        copy_scenario_assets()
