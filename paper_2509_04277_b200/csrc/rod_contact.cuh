@@ -197,4 +197,17 @@ __device__ __forceinline__ void contact_impulse(const StepArgs<Real>& A, int64_t
     }
 }
 
+// The impulse on a velocity held in shared memory, out of line: the contact
+// phase runs only for scenes with contacts, and inlining it would cost every
+// step kernel registers.
+template <typename Real>
+__device__ __noinline__ void contact_impulse_at(const StepArgs<Real>& A, int64_t p, Real m, Real* vx, Real* vy,
+                                                Real* vz) {
+    Real v[3] = {*vx, *vy, *vz};
+    contact_impulse(A, p, m, v);
+    *vx = v[0];
+    *vy = v[1];
+    *vz = v[2];
+}
+
 }  // namespace rsb

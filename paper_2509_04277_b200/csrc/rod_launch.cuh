@@ -7,8 +7,8 @@
 
 #include "rod_step.cuh"
 
-#if !defined(RSB_MODE_NS) || !defined(RSB_MODE_ID)
-#error "define RSB_MODE_NS and RSB_MODE_ID before including rod_launch.cuh"
+#if !defined(RSB_MODE_NS) || !defined(RSB_MODE_ID) || !defined(RSB_FEAT)
+#error "define RSB_MODE_NS, RSB_MODE_ID and RSB_FEAT before including rod_launch.cuh"
 #endif
 
 namespace rsb {
@@ -20,7 +20,10 @@ namespace RSB_MODE_NS {
 //   V0 (1,132)  V1 (1,258)  V2 (1,514)  V3 (2,770)  V4 (4,1154)
 //   V5 (1,130) and V6 (2,130): batches of 129-point rods, 5 CTAs per SM
 //   V7 (2,136): the same without the TMA staging buffer, 8 CTAs per SM
-// Cluster tier: V0, V1, V2, V4; grid tier: V2, V4.
+// Cluster tier: V0, V1, V2, V4; grid tier: V2, V4.  Each precision mode is
+// compiled twice (RSB_FEAT 0 / 1): without and with the contact and
+// self-collision phases; the feature TUs carry the CTA V0-V2, V4, cluster and
+// grid variants only (the planner keeps such scenes on those).
 
 template <typename Real, int S, int CAP, int TIER, int UNI>
 static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
@@ -91,19 +94,27 @@ static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out
 }
 
 // what: 0 = launch, 1 = occupancy query
-// uni: 0 per-slot constants, 1 CTA-uniform (registers), 2 launch-uniform
-// (kernel parameters)
+// cfg = uni + 3 feat.  uni: material constants 0 per slot, 1 CTA-uniform
+// (registers), 2 launch-uniform (kernel parameters); feat: the scene has
+// mesh contacts or self-collision (those phases are compiled only into the
+// feat kernels -- they cost the plain step registers).  The stream tier has
+// no feat kernels (the planner keeps such scenes off it).
 template <typename Real, int S, int CAP, int TIER>
-static cudaError_t dispatch_uni(int what, int uni, const StepArgs<Real>* a, int ncta, int threads,
+static cudaError_t dispatch_uni(int what, int cfg, const StepArgs<Real>* a, int ncta, int threads,
                                 size_t smem, int cluster, cudaStream_t st, int* out) {
-    if (what == 0) {
-        if (uni == 2) return launch_one<Real, S, CAP, TIER, 2>(*a, ncta, threads, smem, cluster, st);
-        if (uni == 1) return launch_one<Real, S, CAP, TIER, 1>(*a, ncta, threads, smem, cluster, st);
-        return launch_one<Real, S, CAP, TIER, 0>(*a, ncta, threads, smem, cluster, st);
+    // this translation unit holds cfg 3 RSB_FEAT .. 3 RSB_FEAT + 2
+    constexpr int C0 = 3 * RSB_FEAT;
+#define RSB_U(C)                                                                                          \
+    case C:                                                                                               \
+        return what == 0 ? launch_one<Real, S, CAP, TIER, C0 + C>(*a, ncta, threads, smem, cluster, st) \
+                         : occupancy_one<Real, S, CAP, TIER, C0 + C>(threads, smem, cluster, out);
+    switch (cfg - C0) {
+        RSB_U(0)
+        RSB_U(1)
+        RSB_U(2)
     }
-    if (uni == 2) return occupancy_one<Real, S, CAP, TIER, 2>(threads, smem, cluster, out);
-    if (uni == 1) return occupancy_one<Real, S, CAP, TIER, 1>(threads, smem, cluster, out);
-    return occupancy_one<Real, S, CAP, TIER, 0>(threads, smem, cluster, out);
+#undef RSB_U
+    return cudaErrorInvalidValue;
 }
 
 template <typename Real>
@@ -111,6 +122,17 @@ static cudaError_t dispatch(int what, int variant, int tier, int uni, const Step
                             int ncta, int threads, size_t smem, int cluster, cudaStream_t st,
                             int* out) {
 #define RSB_D(S, CAP, TIER) dispatch_uni<Real, S, CAP, TIER>(what, uni, a, ncta, threads, smem, cluster, st, out)
+#if RSB_FEAT
+    // scenes with contacts / self-collision: plain CTA, cluster, grid only
+    if (tier == TIER_CTA) {
+        switch (variant) {
+            case 0: return RSB_D(1, 132, TIER_CTA);
+            case 1: return RSB_D(1, 258, TIER_CTA);
+            case 2: return RSB_D(1, 514, TIER_CTA);
+            case 4: return RSB_D(4, 1154, TIER_CTA);
+        }
+    }
+#else
     if (tier == TIER_CTA) {
         switch (variant) {
             case 0: return RSB_D(1, 132, TIER_CTA);
@@ -128,7 +150,9 @@ static cudaError_t dispatch(int what, int variant, int tier, int uni, const Step
             case 6: return RSB_D(2, 130, TIER_STREAM);
             case 7: return RSB_D(2, 136, TIER_STREAM);
         }
-    } else if (tier == TIER_CLUSTER) {
+    }
+#endif
+    if (tier == TIER_CLUSTER) {
         switch (variant) {
             case 0: return RSB_D(1, 132, TIER_CLUSTER);
             case 1: return RSB_D(1, 258, TIER_CLUSTER);

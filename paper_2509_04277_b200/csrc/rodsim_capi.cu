@@ -25,20 +25,23 @@
 #include "rod_common.h"
 #include "rod_step.cuh"
 
-namespace rsb {
-namespace mirror {
-template <typename Real>
-cudaError_t launch_step(int, int, int, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
-template <typename Real>
-cudaError_t occupancy(int, int, int, int, size_t, int, int*);
-}  // namespace mirror
-namespace fast {
-template <typename Real>
-cudaError_t launch_step(int, int, int, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t);
-template <typename Real>
-cudaError_t occupancy(int, int, int, int, size_t, int, int*);
-}  // namespace fast
-}  // namespace rsb
+// launchers of the six kernel translation units (csrc/rod_kernels.cu)
+#define RSB_DECLARE_MODE(NS)                                                                       \
+    namespace rsb {                                                                                \
+    namespace NS {                                                                                 \
+    template <typename Real>                                                                       \
+    cudaError_t launch_step(int, int, int, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t); \
+    template <typename Real>                                                                       \
+    cudaError_t occupancy(int, int, int, int, size_t, int, int*);                                 \
+    }                                                                                              \
+    }
+RSB_DECLARE_MODE(mirror)
+RSB_DECLARE_MODE(mirror_feat)
+RSB_DECLARE_MODE(f32)
+RSB_DECLARE_MODE(f32_feat)
+RSB_DECLARE_MODE(f64fast)
+RSB_DECLARE_MODE(f64fast_feat)
+#undef RSB_DECLARE_MODE
 
 using namespace rsb;
 
@@ -284,15 +287,24 @@ int64_t rod_of(const rs_world_desc& d, int64_t p) {
 
 // ---- launch planning --------------------------------------------------------
 
+// kernel configuration: material-constant storage + scene features
+int launch_cfg(rs_handle h, const Group& g) {
+    const bool feat = (h->contacts_on || h->d.has_self) && g.tier != TIER_STREAM;
+    return g.uni + (feat ? 3 : 0);
+}
+
 int occupancy_query(rs_handle h, int variant, int tier, int uni, int threads, size_t smem,
                     int cluster, int* out) {
     cudaError_t e;
     if (h->prec == RS_F64_MIRROR)
-        e = mirror::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
+        e = uni >= 3 ? mirror_feat::occupancy<double>(variant, tier, uni, threads, smem, cluster, out)
+                     : mirror::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
     else if (h->prec == RS_F32)
-        e = fast::occupancy<float>(variant, tier, uni, threads, smem, cluster, out);
+        e = uni >= 3 ? f32_feat::occupancy<float>(variant, tier, uni, threads, smem, cluster, out)
+                     : f32::occupancy<float>(variant, tier, uni, threads, smem, cluster, out);
     else
-        e = fast::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
+        e = uni >= 3 ? f64fast_feat::occupancy<double>(variant, tier, uni, threads, smem, cluster, out)
+                     : f64fast::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "occupancy query failed: %s", cudaGetErrorString(e));
     return RS_OK;
@@ -658,7 +670,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                         var.CAP, max_np);
         // batches of whole single rods with no bindings: persistent stream
         // tier (TMA prefetch of the next rod while the current one steps)
-        if (g.tier == TIER_CTA && g.variant >= 5 && d.force_tier < 0 &&
+        if (g.tier == TIER_CTA && g.variant >= 5 && d.force_tier < 0 && !h->contacts_on &&
             (colours_aligned || !paired(var.S))) {
             bool single = true;
             for (int t = g.task_begin; t < g.task_begin + g.ncta && single; ++t)
@@ -687,7 +699,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         g.grid = g.tier == TIER_STREAM ? std::min(g.ncta, min_blocks(var.S, var.CAP) * h->num_sms) : g.ncta;
         if (h->dry) continue;
         int occ = 0;
-        int rc = occupancy_query(h, g.variant, g.tier, g.uni, g.threads, g.smem, g.cluster, &occ);
+        int rc = occupancy_query(h, g.variant, g.tier, launch_cfg(h, g), g.threads, g.smem, g.cluster, &occ);
         if (rc) return rc;
         if (g.tier == TIER_CLUSTER && occ < 1)
             return fail(RS_E_UNSUPPORTED, "a %d-CTA cluster of %zu B smem cannot be resident", g.cluster, g.smem);
@@ -757,10 +769,23 @@ int build_grabs(rs_handle h) {
     return put_vec(h, h->tasks, h->h_tasks);
 }
 
+// Contact slots: only a mesh, or slots set by hand, make the contact
+// machinery do anything (every step resets the accumulators and, on
+// detection steps, the slots, _core.pyx:730-741).  Hand-set slots in a world
+// without a mesh are seen at bind time / the next RS_STATIC upload.
+bool contacts_needed(const rs_world_desc& d) {
+    bool on = d.has_mesh != 0;
+    for (int64_t i = 0; i < d.P && !on; ++i)
+        on = d.cact[i] != 0 || d.cacc_n[i] != 0.0 || d.cacc_t[i] != 0.0 || std::signbit(d.cacc_n[i]) ||
+             std::signbit(d.cacc_t[i]);
+    return on;
+}
+
 int upload_static(rs_handle h) {
     const rs_world_desc& d = h->d;
     std::vector<uint32_t> pflags;
     std::vector<int32_t> pt_elem;
+    h->contacts_on = contacts_needed(d);
     int rc = plan(h, pflags, pt_elem);
     if (rc) return rc;
     const size_t P = size_t(d.P), E = size_t(d.E), R = size_t(d.R);
@@ -819,15 +844,7 @@ int upload_static(rs_handle h) {
         if ((rc = put_i32(h, h->grp_e, d.grp_e, size_t(d.n_groups)))) return rc;
         if ((rc = dev_alloc(h->grp_c, h->rsz * 3 * size_t(d.n_groups)))) return rc;
     }
-    // contact slots: only a mesh, or slots set by hand, make the contact
-    // machinery do anything (every step resets the accumulators and, on
-    // detection steps, the slots, _core.pyx:730-741).  Hand-set slots in a
-    // world without a mesh are seen at bind time / the next RS_STATIC upload.
-    bool on = d.has_mesh != 0;
-    for (size_t i = 0; i < P && !on; ++i)
-        on = d.cact[i] != 0 || d.cacc_n[i] != 0.0 || d.cacc_t[i] != 0.0 || std::signbit(d.cacc_n[i]) ||
-             std::signbit(d.cacc_t[i]);
-    h->contacts_on = on;
+
     if ((rc = put_real(h, h->cradii, d.cradii, P))) return rc;
     if ((rc = put_u8(h, h->cmask, d.cmask, P))) return rc;
     if ((rc = put_vec(h, h->binds, h->h_binds))) return rc;
@@ -1026,18 +1043,22 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         a.ntasks = nt;
     };
     cudaError_t e;
+    const int cfg = launch_cfg(h, g);
     if (h->prec == RS_F64_MIRROR) {
         auto a = make_args<double>(h, g, step0, steps);
         sub(a);
-        e = mirror::launch_step<double>(g.variant, g.tier, g.uni, a, grid, g.threads, g.smem, g.cluster, h->st);
+        e = cfg >= 3 ? mirror_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
+                     : mirror::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
     } else if (h->prec == RS_F32) {
         auto a = make_args<float>(h, g, step0, steps);
         sub(a);
-        e = fast::launch_step<float>(g.variant, g.tier, g.uni, a, grid, g.threads, g.smem, g.cluster, h->st);
+        e = cfg >= 3 ? f32_feat::launch_step<float>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
+                     : f32::launch_step<float>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
     } else {
         auto a = make_args<double>(h, g, step0, steps);
         sub(a);
-        e = fast::launch_step<double>(g.variant, g.tier, g.uni, a, grid, g.threads, g.smem, g.cluster, h->st);
+        e = cfg >= 3 ? f64fast_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
+                     : f64fast::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
     }
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
@@ -1483,6 +1504,7 @@ int rs_plan_dry(const rs_world_desc* desc, int32_t num_sms, char* buf, int64_t l
     h.rsz = h.prec == RS_F32 ? sizeof(float) : sizeof(double);
     h.num_sms = num_sms;
     h.dry = true;
+    h.contacts_on = contacts_needed(*desc);
     std::vector<uint32_t> pflags;
     std::vector<int32_t> pt_elem;
     int rc = plan(&h, pflags, pt_elem);
@@ -1501,15 +1523,10 @@ int rs_device_ptr(rs_handle h, int32_t which, void** out) {
 }  // extern "C"
 
 namespace rsb {
-namespace mirror {
+namespace micro {   // csrc/rod_micro.cu
 cudaError_t div_selftest(const double*, const double*, int64_t, double*, double*);
-}
-}  // namespace rsb
-
-namespace rsb {
-namespace fast {
 cudaError_t pipe_peak(int kind, int blocks, int threads, int iters, float* ms, double* ops);
-}
+}  // namespace micro
 }  // namespace rsb
 
 extern "C" int rs_pipe_peak(int kind, double* ops_per_s) {
@@ -1518,7 +1535,7 @@ extern "C" int rs_pipe_peak(int kind, double* ops_per_s) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     float ms = 0.f;
     double ops = 0.0;
-    CK(rsb::fast::pipe_peak(kind, sms * 8, 256, 4096, &ms, &ops));
+    CK(rsb::micro::pipe_peak(kind, sms * 8, 256, 4096, &ms, &ops));
     *ops_per_s = ops / (double(ms) * 1e-3);
     return RS_OK;
 }
@@ -1533,7 +1550,7 @@ extern "C" int rs_selftest_div(const double* a, const double* b, int64_t n, doub
     CK(cudaMalloc(&df, bytes));
     CK(cudaMemcpy(da, a, bytes, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(db, b, bytes, cudaMemcpyHostToDevice));
-    CK(rsb::mirror::div_selftest(da, db, n, dq, df));
+    CK(rsb::micro::div_selftest(da, db, n, dq, df));
     CK(cudaMemcpy(q_ieee, dq, bytes, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(q_fast, df, bytes, cudaMemcpyDeviceToHost));
     cudaFree(da);

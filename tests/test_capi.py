@@ -167,3 +167,11 @@ def test_desc_binds_the_mesh_tree():
     assert keep["tris"].dtype == np.int64 and keep["cact"] is w.contact_active
     p = _lib.plan_dry(w)
     assert p["groups"][0]["tier"] == "cta"
+
+
+def test_contact_batches_stay_off_the_stream_tier():
+    from paper_2509_04277_b200 import bvh, meshes
+    w = wl.hair(2048)
+    assert plan(w)[0]["tier"] == "stream"
+    w.set_mesh(bvh.build_aabb_tree(*meshes.floor_mesh(y=-1.0, cells=2)))
+    assert plan(w)[0]["tier"] == "cta"
