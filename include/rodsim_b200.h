@@ -118,6 +118,12 @@ typedef struct rs_world_desc {
     double touch, broad;              /* 2 point_radius, 2 sphere_radius */
     int64_t *pair_a, *pair_b;         /* (pair_cap) */
     double *pair_md, *pair_acc;       /* (pair_cap) */
+    /* 1: live launches -- for a plan of one CTA or one cluster the kernel
+     * drains staged commands at every step boundary, so commands staged while
+     * an epoch runs apply at the next step (the reference's parallel backend,
+     * engine.py:177-198); 0: they apply at the next epoch.  Live launches use
+     * the heavier scene-feature kernels. */
+    int64_t live;
 } rs_world_desc;
 
 typedef struct rs_handle_s *rs_handle;

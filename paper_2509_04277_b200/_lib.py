@@ -69,6 +69,7 @@ class WorldDesc(ctypes.Structure):
         ("grp_rod", _p), ("grp_gi", _p), ("grp_s", _p), ("grp_e", _p),
         ("touch", _f64), ("broad", _f64),
         ("pair_a", _p), ("pair_b", _p), ("pair_md", _p), ("pair_acc", _p),
+        ("live", _i64),
     ]
 
 
@@ -165,7 +166,7 @@ def _ptr(a):
 
 
 def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
-               force_variant=-1):
+               force_variant=-1, live=False):
     """`rs_world_desc` over the World's arrays (bound by pointer, like
     make_context, _core.pyx:219-403) plus the dict keeping them alive."""
     w = world
@@ -245,6 +246,7 @@ def build_desc(world, precision="f64", device=0, force_tier=-1, force_ctas=0,
     d.coll_margin = float(w.collision_margin)
     d.restitution = float(w.solver.restitution)
     d.mu = float(w.solver.mu)
+    d.live = int(bool(live))
     if cfg is not None:
         d.has_self = 1
         d.n_groups = arrays["grp_rod"].shape[0]
@@ -274,12 +276,12 @@ class DeviceWorld:
     """
 
     def __init__(self, world, precision="f64", device=0, force_tier=-1,
-                 force_ctas=0, force_variant=-1):
+                 force_ctas=0, force_variant=-1, live=False):
         self.lib = load_library()
         self.world = world
         self.precision = precision
         self.desc, self.arrays = build_desc(world, precision, device, force_tier,
-                                            force_ctas, force_variant)
+                                            force_ctas, force_variant, live)
         d = self.desc
         h = _p()
         check(self.lib.rs_create(ctypes.byref(d), ctypes.byref(h)), self.lib)

@@ -81,6 +81,19 @@ struct UniConsts {
     Real kb[3], us[3], I[3], rI[3];  // bend/twist stiffness, u*, inertia, 1/inertia
 };
 
+// The staged-command ring (_core.pyx:1151-1184, ph_boundary 477-506) in
+// page-locked, device-mapped host memory: the host appends rows and
+// publishes `tail`; the drainer -- the host at an epoch boundary, or, in a
+// live launch, the step kernel at every step boundary -- applies rows in
+// order, stamps each row's apply step and publishes `head`.
+constexpr int RING_CAP = 64;
+struct LiveRing {
+    int64_t tail;                   // rows published by the host
+    int64_t head;                   // rows applied
+    int64_t apply[RING_CAP];        // core step each row was applied at (-1: not yet)
+    double rows[RING_CAP][6];       // [op, i0, i1, f0, f1, f2]
+};
+
 // Kernel arguments; device pointers, AoS layouts identical to world.py.
 template <typename Real>
 struct StepArgs {
@@ -131,6 +144,13 @@ struct StepArgs {
     int32_t *pair_a, *pair_b, *pair_count;         // pair list, CNT_PAIRS (persistent)
     Real *pair_md, *pair_acc;
     Real touch, broad;
+    // live launch (single CTA / single cluster): commands drained at every
+    // step boundary from the mapped ring into the device control arrays
+    LiveRing* live;                                // null: not live
+    Real *drv_v_live, *drv_rot_live;               // = drv_v / drv_rot, writable
+    int32_t *g_act, *g_pt;                         // (ngrab) world grab slots
+    Real* g_tgt;                                   // (ngrab,3)
+    int32_t ngrab, nrods;
 };
 
 constexpr int PROF_SLOTS = 64;

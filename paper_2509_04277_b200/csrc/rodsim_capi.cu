@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -86,7 +87,6 @@ constexpr int kBatchVariant = 7;   // batches of short rods; 5 and 6 on request
 constexpr int kClusterVariants[] = {0, 1, 2, 4};
 constexpr int kCtaMaxPoints = 513;   // variant 2 covers 512 slots + the tail
 constexpr int kMaxCluster = 16;
-constexpr int kRingCap = 64;
 constexpr int kMaxStepsPerLaunch = 1 << 16;
 constexpr size_t kMaxSmem = 232448;   // 227 KB opt-in per CTA on sm_100
 
@@ -169,9 +169,11 @@ struct rs_handle_s {
     int64_t step = 0;
     int64_t err_step = -1;
     std::mutex ring_mu;
-    double ring[kRingCap][6];
-    int64_t ring_apply[kRingCap];
-    int64_t head = 0, tail = 0;
+    LiveRing* ring = nullptr;       // page-locked, device-mapped (rod_common.h)
+    LiveRing* ring_dev = nullptr;   // its device address
+    bool live = false;              // the plan is one CTA / one cluster: the
+                                    // kernel drains the ring at every step
+    DevBuf g_act_d, g_pt_d, g_tgt_d;   // world grab slots on the device (live)
     bool control_dirty = false;
     // last uploaded controls (upload_control skips unchanged ones)
     bool ctl_valid = false;
@@ -289,7 +291,7 @@ int64_t rod_of(const rs_world_desc& d, int64_t p) {
 
 // kernel configuration: material-constant storage + scene features
 int launch_cfg(rs_handle h, const Group& g) {
-    const bool feat = (h->contacts_on || h->d.has_self) && g.tier != TIER_STREAM;
+    const bool feat = (h->contacts_on || h->d.has_self || h->live) && g.tier != TIER_STREAM;
     return g.uni + (feat ? 3 : 0);
 }
 
@@ -728,6 +730,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     for (size_t gi = 0; gi < h->groups.size(); ++gi)
         for (int t = h->groups[gi].task_begin; t < h->groups[gi].task_begin + h->groups[gi].ncta; ++t)
             h->task_group[t] = int(gi);
+    // one CTA or one cluster: the kernel itself drains staged commands at
+    // every step boundary (commands posted while an epoch runs apply at the
+    // next step, like the reference's parallel backend)
+    h->live = d.live != 0 && h->groups.size() == 1 &&
+              ((h->groups[0].tier == TIER_CTA && h->groups[0].ncta == 1 && h->groups[0].variant <= 4 &&
+                h->groups[0].variant != 3) ||
+               h->groups[0].tier == TIER_CLUSTER);
     h->planned = true;
     return RS_OK;
 }
@@ -873,6 +882,13 @@ int upload_control(rs_handle h) {
     int rc = put_real(h, h->drv_v, d.drv_v, 3 * size_t(d.R));
     if (rc) return rc;
     if ((rc = put_real(h, h->drv_rot, d.drv_rot, size_t(d.R)))) return rc;
+    {   // the world's grab slots, as the live kernel drains commands into them
+        std::vector<int64_t> act(G);
+        for (size_t g = 0; g < G; ++g) act[g] = d.g_act[g];
+        if ((rc = put_i32(h, h->g_act_d, act.data(), G))) return rc;
+        if ((rc = put_i32(h, h->g_pt_d, d.g_pt, G))) return rc;
+        if ((rc = put_real(h, h->g_tgt_d, d.g_tgt, 3 * G))) return rc;
+    }
     if (!h->planned) return RS_OK;
     return build_grabs(h);
 }
@@ -899,13 +915,16 @@ int upload_state(rs_handle h) {
     return put_real(h, h->cacc_t, d.cacc_t, P);
 }
 
-// Apply staged commands at the step boundary (ph_boundary, _core.pyx:477-506).
+// Apply staged commands at the step boundary (ph_boundary, _core.pyx:477-506)
+// -- the host's drain, for launches that are not live.
 void drain_ring(rs_handle h) {
     std::lock_guard<std::mutex> lk(h->ring_mu);
     rs_world_desc& d = h->d;
-    while (h->head < h->tail) {
-        const int slot = int(h->head % kRingCap);
-        const double* r = h->ring[slot];
+    volatile LiveRing* R = h->ring;
+    while (R->head < R->tail) {
+        const int slot = int(R->head % RING_CAP);
+        double r[6];
+        for (int k = 0; k < 6; ++k) r[k] = R->rows[slot][k];
         const int op = int(r[0]);
         const int64_t i0 = int64_t(r[1]), i1 = int64_t(r[2]);
         if (op == 0 && i0 >= 0 && i0 < d.R) {
@@ -920,8 +939,8 @@ void drain_ring(rs_handle h) {
             d.g_act[i0] = 0;
             d.g_pt[i0] = -1;
         }
-        h->ring_apply[slot] = h->step;
-        h->head += 1;
+        R->apply[slot] = h->step;
+        R->head = R->head + 1;
         h->control_dirty = true;
     }
 }
@@ -1018,6 +1037,14 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.pair_md = static_cast<Real*>(h->pair_md.p);
     a.pair_acc = static_cast<Real*>(h->pair_acc.p);
     a.pair_count = h->d_pairs;
+    a.live = h->live ? h->ring_dev : nullptr;
+    a.drv_v_live = static_cast<Real*>(h->drv_v.p);
+    a.drv_rot_live = static_cast<Real*>(h->drv_rot.p);
+    a.g_act = static_cast<int32_t*>(h->g_act_d.p);
+    a.g_pt = static_cast<int32_t*>(h->g_pt_d.p);
+    a.g_tgt = static_cast<Real*>(h->g_tgt_d.p);
+    a.ngrab = int32_t(h->d.ngrab);
+    a.nrods = int32_t(h->d.R);
     a.touch = Real(h->d.touch);
     a.broad = Real(h->d.broad);
     a.coll_margin = Real(h->d.coll_margin);
@@ -1079,7 +1106,7 @@ void register_host(rs_handle h, void* p, size_t bytes) {
 
 // ph_boundary at the epoch's first step: staged commands, dirty controls
 int epoch_prelude(rs_handle h) {
-    drain_ring(h);
+    if (!h->live) drain_ring(h);   // live launches drain in the kernel
     if (h->control_dirty) {
         int rc = upload_control(h);
         if (rc) return rc;
@@ -1195,7 +1222,15 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     h->rsz = h->prec == RS_F32 ? sizeof(float) : sizeof(double);
     h->step = desc->step_index;
     if (const char* dbg = getenv("RSB_DEBUG")) h->debug = atoi(dbg);
-    for (int i = 0; i < kRingCap; ++i) h->ring_apply[i] = -1;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&h->ring), sizeof(LiveRing), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->ring_dev), h->ring, 0) != cudaSuccess) {
+        cudaGetLastError();
+        h->ring = nullptr;
+        delete h;
+        return fail(RS_E_CUDA, "mapped command ring allocation failed");
+    }
+    std::memset(h->ring, 0, sizeof(LiveRing));
+    for (int i = 0; i < RING_CAP; ++i) h->ring->apply[i] = -1;
     int rc = RS_OK;
     auto bail = [&](int code) {
         rs_destroy(h);
@@ -1287,11 +1322,37 @@ int rs_synchronize(rs_handle h) {
     return RS_OK;
 }
 
+// After a live epoch the device holds the authoritative driver and grab
+// slots (commands were applied to them mid-launch): copy them back into the
+// World's arrays, which the reference mutates in place.
+int download_control(rs_handle h) {
+    const rs_world_desc& d = h->d;
+    const size_t R = size_t(d.R), G = size_t(d.ngrab);
+    int rc = get_real(h, h->drv_v, d.drv_v, 3 * R);
+    if (rc) return rc;
+    if ((rc = get_real(h, h->drv_rot, d.drv_rot, R))) return rc;
+    if ((rc = get_real(h, h->g_tgt_d, d.g_tgt, 3 * G))) return rc;
+    std::vector<int32_t> act(G), pt(G);
+    if (G) {
+        CK(cudaMemcpyAsync(act.data(), h->g_act_d.p, G * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(pt.data(), h->g_pt_d.p, G * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    for (size_t g = 0; g < G; ++g) {
+        d.g_act[g] = uint8_t(act[g] != 0);
+        d.g_pt[g] = pt[g];
+    }
+    h->ctl_valid = false;   // re-sync the upload cache with what is now on the host
+    return RS_OK;
+}
+
 int rs_download(rs_handle h, uint32_t mask) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     CK(cudaSetDevice(h->d.device));
     const rs_world_desc& d = h->d;
     int rc = RS_OK;
+    if ((mask & (RS_STATE | RS_CONTROL)) && h->live && h->planned)
+        if ((rc = download_control(h))) return rc;
     if (mask & RS_STATE) {
         if ((rc = get_real(h, h->pos, d.pos, 3 * size_t(d.P)))) return rc;
         if ((rc = get_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
@@ -1361,22 +1422,27 @@ int rs_update_params(rs_handle h, double dt, int64_t iters) {
 int rs_stage_commands(rs_handle h, const double* ops, int64_t n, int64_t* slots) {
     if (!h || (n > 0 && !ops)) return fail(RS_E_INVALID, "null argument");
     std::lock_guard<std::mutex> lk(h->ring_mu);
+    volatile LiveRing* R = h->ring;
     for (int64_t i = 0; i < n; ++i) {
-        if (h->tail - h->head >= kRingCap)
-            return fail(RS_E_RING_FULL, "command ring full and not draining");
-        const int slot = int(h->tail % kRingCap);
-        h->ring_apply[slot] = -1;
-        std::memcpy(h->ring[slot], ops + 6 * i, 6 * sizeof(double));
-        if (slots) slots[i] = h->tail;
-        h->tail += 1;
+        const int64_t tail = R->tail;
+        if (tail - R->head >= RING_CAP) return fail(RS_E_RING_FULL, "command ring full and not draining");
+        const int slot = int(tail % RING_CAP);
+        R->apply[slot] = -1;
+        for (int k = 0; k < 6; ++k) R->rows[slot][k] = ops[6 * i + k];
+        if (slots) slots[i] = tail;
+        // rows before tail (x86 stores are ordered; the fence keeps the
+        // compiler from reordering them)
+        std::atomic_thread_fence(std::memory_order_release);
+        R->tail = tail + 1;
     }
     return RS_OK;
 }
 
 int64_t rs_applied_step_for(rs_handle h, int64_t global_slot) {
     if (!h) return -1;
-    std::lock_guard<std::mutex> lk(h->ring_mu);
-    return h->ring_apply[global_slot % kRingCap];
+    volatile LiveRing* R = h->ring;
+    if (global_slot < 0 || global_slot >= R->tail || global_slot < R->tail - RING_CAP) return -1;
+    return R->apply[global_slot % RING_CAP];
 }
 
 int rs_read_snapshot(rs_handle h, double* pos, double* q, int64_t* seq, int64_t* step) {
@@ -1398,7 +1464,8 @@ void rs_destroy(rs_handle h) {
                       &h->pt_elem, &h->tasks, &h->binds, &h->drvs, &h->grabs, &h->nmin, &h->nmax, &h->verts,
                       &h->nstart, &h->ncount, &h->torder, &h->tris, &h->cradii, &h->cmask, &h->cact, &h->cnorm,
                       &h->cdepth, &h->cacc_n, &h->cacc_t, &h->grp_rod, &h->grp_gi, &h->grp_s, &h->grp_e,
-                      &h->grp_c, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc})
+                      &h->grp_c, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc, &h->g_act_d, &h->g_pt_d,
+                      &h->g_tgt_d})
         if (b->p) cudaFree(b->p);
     for (Group& g : h->groups) {
         if (g.d_flags) cudaFree(g.d_flags);
@@ -1424,6 +1491,7 @@ void rs_destroy(rs_handle h) {
     if (h->d_pairs) cudaFree(h->d_pairs);
     if (h->h_contacts) cudaFreeHost(h->h_contacts);
     if (h->stage) cudaFreeHost(h->stage);
+    if (h->ring) cudaFreeHost(h->ring);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->tm0) cudaEventDestroy(h->tm0);
@@ -1488,7 +1556,7 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
                  g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap);
         s += tmp;
     }
-    s += "]}";
+    s += std::string("], \"live\": ") + (h->live ? "true" : "false") + "}";
     if (int64_t(s.size()) + 1 > len) return fail(RS_E_INVALID, "buffer too small");
     std::memcpy(buf, s.c_str(), s.size() + 1);
     return RS_OK;

@@ -162,7 +162,7 @@ class Engine:
 
     def __init__(self, world, backend="serial", block_cap=512,
                  use_compiled=None, max_blocks=None, precision="f64",
-                 device=0, force_tier=-1, force_ctas=0, force_variant=-1):
+                 device=0, force_tier=-1, force_ctas=0, force_variant=-1, live=None):
         if backend not in ("serial", "parallel"):
             raise ValueError("backend must be 'serial' or 'parallel'")
         self.world = world
@@ -178,7 +178,13 @@ class Engine:
         self.compiled = True       # the CUDA core is the only backend
         self._pending = []
         self._force = (force_tier, force_ctas, force_variant)
+        # live launches apply commands posted mid-epoch at the next step (the
+        # reference's parallel backend); default: on for backend="parallel"
+        self._want_live = (backend == "parallel") if live is None else bool(live)
         self._lock = threading.Lock()
+        self._stage_lock = threading.Lock()
+        self._running = False      # an epoch's launch is in flight
+        self._live = False
         self._snapshot_readers = False
         self._snapshot_stale = False
         self._dev = None
@@ -193,7 +199,8 @@ class Engine:
         ft, fc, fv = self._force
         self._dev = _lib.DeviceWorld(self.world, self.precision, self.device,
                                      force_tier=ft, force_ctas=fc,
-                                     force_variant=fv)
+                                     force_variant=fv, live=self._want_live)
+        self._live = bool(self._dev.plan().get("live", False))
         self._bound = {a: getattr(self.world, a) for a in _BOUND_ATTRS}
         # the mesh and the collision scalars are bound too (make_context)
         self._bound_scene = self._scene_key()
@@ -234,7 +241,27 @@ class Engine:
     # -- commands ----------------------------------------------------------
 
     def post_command(self, name, **args):
-        return self.mailbox.post(name, **args)
+        """Queue a command.  Between epochs it applies at the next epoch's
+        first step boundary; while an epoch runs on a live plan (one CTA or
+        one cluster) it is staged on the device ring right away and the
+        kernel applies it at the next step boundary, like the reference's
+        parallel backend (engine.py:177-198)."""
+        ticket = self.mailbox.post(name, **args)
+        if self._running and self._live:
+            self._stage_pending()
+        return ticket
+
+    def _stage_pending(self):
+        """Encode queued commands onto the device ring (_core.stage_commands);
+        their tickets resolve once the kernel reports the apply step."""
+        with self._stage_lock:
+            for cmd, ticket in self.mailbox.drain():
+                ops = self._encode(cmd)
+                if not ops:
+                    ticket.resolve(self.world.step_index)
+                    continue
+                slots = self._dev.stage_commands(np.array(ops, dtype=np.float64))
+                self._pending.append((cmd, ticket, slots[-1]))
 
     def _encode(self, cmd):
         """Command -> [op, i0, i1, f0, f1, f2] rows (engine.py:200-226)."""
@@ -318,12 +345,20 @@ class Engine:
             raise ValueError("steps must be >= 1")
         with self._lock:
             t0 = time.perf_counter_ns()
-            self._drain_at_boundary()
-            if self._push(state=False):
-                contacts, barrier_ns = self._dev.run_host(steps)
-            else:   # re-bound: the state was just uploaded
-                contacts, barrier_ns = self._dev.run(steps)
-                self._dev.download(_lib.RS_STATE)
+            with self._stage_lock:
+                self._drain_at_boundary()
+            pushed = self._push(state=False)
+            self._running = True
+            try:
+                if self._live:   # posted just before the launch: the kernel drains them
+                    self._stage_pending()
+                if pushed:
+                    contacts, barrier_ns = self._dev.run_host(steps)
+                else:   # re-bound: the state was just uploaded
+                    contacts, barrier_ns = self._dev.run(steps)
+                    self._dev.download(_lib.RS_STATE)
+            finally:
+                self._running = False
             self.world.step_index += steps
             self._resolve_applied()
             self.last_contacts = contacts

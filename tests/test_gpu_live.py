@@ -1,0 +1,97 @@
+"""Live commands: with Engine(live=True) (the default
+for backend="parallel"), a command posted from another thread while a long
+epoch runs on a one-CTA or one-cluster plan is drained
+by the kernel at the next step boundary -- its ticket reports that step --
+and the state equals, bit for bit, the oracle run with the command applied
+at exactly that step (_core.pyx:477-506, engine.py:177-198)."""
+
+import threading
+import time
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleStepper
+from paper_2509_04277_b200 import workloads as wl
+from paper_2509_04277_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+STATE = ("positions", "velocities", "frames", "angular_velocities")
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.int64)
+
+
+def live_run(make, steps, post):
+    """Run one epoch of `steps` in a thread, post commands mid-flight."""
+    g = make()
+    with Engine(g, live=True) as eng:
+        assert eng.plan()["live"]
+        eng.run_epoch(1)                      # bind / warm up
+        box = {}
+
+        def run():
+            try:
+                box["m"] = eng.run_epoch(steps)
+            except Exception as exc:   # surfaced below
+                box["error"] = exc
+        th = threading.Thread(target=run)
+        th.start()
+        tickets = post(eng)
+        th.join()
+        assert "error" not in box, box.get("error")
+        applied = [t.wait(5.0) for t in tickets]
+    return g, applied
+
+
+def test_live_driver_velocity_on_cluster_pair():
+    steps = 4000
+
+    def post(eng):
+        time.sleep(0.02)
+        return [eng.post_command("insert_velocity", rod=0, value=0.2, axis=(0.0, 0.0, 1.0))]
+    g, (s_apply,) = live_run(wl.pair, steps, post)
+    assert 1 < s_apply < 1 + steps          # applied mid-epoch, not at a boundary
+    r = wl.pair()
+    o = OracleStepper(r)
+    o.run(s_apply)
+    r.driver_velocity[0] = (0.0, 0.0, 0.2)
+    o.run(1 + steps - s_apply)
+    assert np.isfinite(r.positions).all()
+    for k in STATE:
+        assert np.array_equal(_bits(getattr(g, k)), _bits(getattr(r, k))), k
+    assert np.array_equal(g.driver_velocity, r.driver_velocity)
+
+
+def test_live_grab_and_release_on_cta():
+    # the knot threads (one CTA, soft and damped): a grab on the second
+    # thread's free end and its release, both posted mid-epoch
+    steps = 6000
+
+    def post(eng):
+        time.sleep(0.01)
+        a = eng.post_command("grab", rod=1, index=47, target=(0.11, 0.005, 0.02))
+        time.sleep(0.02)
+        b = eng.post_command("release", rod=1, index=47)
+        return [a, b]
+    g, (s_grab, s_rel) = live_run(wl.knot, steps, post)
+    assert 1 < s_grab < s_rel < 1 + steps
+    r = wl.knot()
+    o = OracleStepper(r)
+    o.run(s_grab)
+    r.grab(1, 47, np.array([0.11, 0.005, 0.02]))
+    o.run(s_rel - s_grab)
+    r.release(1, 47)
+    o.run(1 + steps - s_rel)
+    assert np.isfinite(r.positions).all()
+    for k in STATE:
+        assert np.array_equal(_bits(getattr(g, k)), _bits(getattr(r, k))), k
+    assert not g.grab_active.any()
+
+
+def test_live_is_opt_in():
+    with Engine(wl.cantilever()) as eng:
+        assert not eng.plan()["live"]
+    with Engine(wl.cantilever(), backend="parallel") as eng:
+        assert eng.plan()["live"]
