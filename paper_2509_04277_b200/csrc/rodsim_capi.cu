@@ -711,7 +711,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         if ((g.tier == TIER_CTA || g.tier == TIER_STREAM) && occ < 1)
             return fail(RS_E_UNSUPPORTED, "CTA plan cannot be resident (%zu B smem, %d threads)", g.smem,
                         g.threads);
-        if (g.tier == TIER_STREAM) g.grid = std::min(g.ncta, occ * h->num_sms);
+        if (g.tier == TIER_STREAM) {
+            // persistent CTAs per SM: the occupancy limit, or fewer on request
+            // (RSB_STREAM_CTAS, tuning experiments)
+            int per_sm = occ;
+            if (const char* e = getenv("RSB_STREAM_CTAS")) per_sm = std::max(1, std::min(occ, atoi(e)));
+            g.grid = std::min(g.ncta, per_sm * h->num_sms);
+        }
         if (g.tier == TIER_GRID) {
             CK(cudaMalloc(&g.d_flags, sizeof(int32_t) * g.ncta));
             CK(cudaMalloc(&g.d_halo, h->rsz * 2 * HALO_WORDS * size_t(g.ncta)));
