@@ -48,3 +48,11 @@ def test_replay_session_matches_run_scenario():
     _, engine = scenarios.run_scenario("knot_replay", scenarios.default_config("knot_replay"),
                                        steps=500, batch=100)
     assert np.array_equal(_bits(w.positions), _bits(engine.world.positions))
+
+
+def test_bench_case_rows(tmp_path):
+    from paper_2509_04277_b200 import bench as rb
+    rows = rb.bench_suite({"n": [33, 600], "batch": [10], "backend": ["serial", "parallel"],
+                           "core": ["compiled", "python"], "epochs": 2})
+    assert len(rows) == 4 and all(r["per_step_ns"] > 0 for r in rows)
+    assert rb.export_rows(rows, str(tmp_path / "b.csv"))
