@@ -190,7 +190,8 @@ int rs_pipe_peak(int kind, double *ops_per_s);
  * 1 DMUL, 2 DFMA, 3 IEEE div, 4 sqrt+add, 5 reciprocal-based div, 6 1/x
  * (dependent chains), 7 shared-memory load chase, 8 bar.sync with `param`
  * threads, 9 barrier.cluster across `param` CTAs (+ one DSMEM read per
- * phase), 10 DSMEM load chase.  out[0] = cycles, out[1] = ns (0 if not
+ * phase), 10 DSMEM load chase, 11 neighbour-only mbarrier sync along a
+ * chain of `param` cluster CTAs (+ one DSMEM read per phase).  out[0] = cycles, out[1] = ns (0 if not
  * measured) per operation / barrier. */
 int rs_micro(int kind, int param, double *out);
 

@@ -112,6 +112,69 @@ __global__ void cluster_bar_kernel(double* out, int iters) {
     if (acc == -1.0) out[2] = acc;
 }
 
+// Neighbour-only synchronisation across a cluster (a chain of CTAs, like a
+// rod split over the cluster): per phase bar.sync, thread 0 arrives on the
+// left and right neighbours' mbarriers (remote, release.cluster) and waits on
+// its own two (acquire.cluster), bar.sync -- with one DSMEM read of the
+// neighbour's slot per phase, as in the cluster barrier benchmark.
+__global__ void nb_sync_kernel(double* out, int iters) {
+    __shared__ __align__(8) uint64_t nbar[2][2];   // [from left / from right][parity]
+    __shared__ double buf[32];
+    unsigned rank, nrank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nrank));
+    const bool has_l = rank > 0, has_r = rank + 1 < nrank;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(&nbar[i / 2][i % 2]))) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 32) buf[threadIdx.x] = rank;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const uint32_t local_buf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+    uint32_t nb_buf;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(nb_buf) : "r"(local_buf), "r"(has_r ? rank + 1 : rank));
+    auto remote_bar = [&](int side, int b, unsigned to) {
+        uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&nbar[side][b])), r;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(to));
+        return r;
+    };
+    double acc = 0;
+    const uint64_t t0 = gtimer();
+    const long long c0 = clock64();
+    for (int ph = 0; ph < iters; ++ph) {
+        double v;
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(nb_buf) : "memory");
+        acc += v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int b = ph & 1;
+            const uint32_t par = (ph >> 1) & 1;
+            if (has_l) asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar(1, b, rank - 1)) : "memory");
+            if (has_r) asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar(0, b, rank + 1)) : "memory");
+            for (int side = 0; side < 2; ++side) {
+                if (side == 0 ? !has_l : !has_r) continue;
+                const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&nbar[side][b]));
+                asm volatile(
+                    "{\n\t.reg .pred p;\n"
+                    "NBW_%=:\n\t"
+                    "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+                    "@!p bra NBW_%=;\n}" ::"r"(a), "r"(par) : "memory");
+            }
+        }
+        __syncthreads();
+    }
+    const long long c1 = clock64();
+    const uint64_t t1 = gtimer();
+    if (rank == 0 && threadIdx.x == 0) {
+        out[0] = double(c1 - c0) / iters;
+        out[1] = double(t1 - t0) / iters;
+    }
+    if (acc == -1.0) out[2] = acc;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // DSMEM dependent remote load latency (thread 0 of rank 0 chases through
 // rank 1's shared memory)
 __global__ void dsmem_kernel(double* out, int iters) {
@@ -158,11 +221,12 @@ cudaError_t run(int kind, int param, double* res) {
             case 7: lds_kernel<<<1, 32>>>(buf, iters); break;
             case 8: bar_kernel<<<1, param>>>(buf, iters); break;
             case 9:
-            case 10: {
+            case 10:
+            case 11: {
                 cudaLaunchConfig_t cfg = {};
-                const int c = kind == 9 ? param : 2;
+                const int c = kind == 10 ? 2 : param;
                 cfg.gridDim = dim3(c);
-                cfg.blockDim = dim3(kind == 9 ? 128 : 32);
+                cfg.blockDim = dim3(kind == 10 ? 32 : 128);
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeClusterDimension;
                 attr[0].val.clusterDim.x = c;
@@ -170,6 +234,10 @@ cudaError_t run(int kind, int param, double* res) {
                 attr[0].val.clusterDim.z = 1;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
+                if (kind == 11) {
+                    if (c > 8) cudaFuncSetAttribute(nb_sync_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                    return cudaLaunchKernelEx(&cfg, nb_sync_kernel, buf, iters);
+                }
                 if (kind == 9) {
                     if (c > 8) cudaFuncSetAttribute(cluster_bar_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                     return cudaLaunchKernelEx(&cfg, cluster_bar_kernel, buf, iters);

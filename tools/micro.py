@@ -20,6 +20,8 @@ def main():
     for c_ in (2, 4, 8, 16):
         c, ns = _lib.micro("cluster_barrier", c_)
         out[f"cluster_barrier_{c_}"] = {"cycles": round(c, 2), "ns": round(ns, 2)}
+        c, ns = _lib.micro("neighbour_sync", c_)
+        out[f"neighbour_sync_{c_}"] = {"cycles": round(c, 2), "ns": round(ns, 2)}
     peaks = {n: _lib.pipe_peak(i) for i, n in enumerate(("dfma", "dadd", "dmul", "ffma"))}
     out["pipe_peak_ops_per_s"] = peaks
     print(json.dumps(out, indent=1))
