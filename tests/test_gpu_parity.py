@@ -336,3 +336,36 @@ def test_fp64_fast_mode_within_1e9():
     OracleStepper(r).run(1000)
     rel = np.max(np.abs(g.positions - r.positions)) / np.max(np.abs(r.positions))
     assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("lo,tier", [(66, "stream"), (2, "cta")])
+def test_mixed_batch_bitwise(lo, tier):
+    # 1500 rods of lo..129 points, every 7th extensible, bending stiffness
+    # varying per rod.  Rods of >= 66 points
+    # cannot share a 129-slot CTA: the persistent stream tier, tasks with and
+    # without a tail slot.  Down to single-element rods they are packed
+    # several per CTA: the CTA tier.
+    def make():
+        rng = np.random.default_rng(11)
+        w = World(dt=1e-4, gravity=(0.0, -9.81, 0.0), solver=SolverConfig(iterations=10))
+        for r in range(1500):
+            n = int(rng.integers(lo, 130))
+            p = st.RodParams(radius=1e-3, stretch_modulus=1e6, bend_modulus=float(rng.uniform(5e5, 2e6)),
+                             shear_modulus=1e6, linear_density=0.05, damping_translational=2e-4,
+                             damping_rotational=1e-8, extensible=(r % 7 == 0))
+            w.add_rod(st.init_rod(n, 2e-3 * (n - 1), axis=(1.0, 0.1 * (r % 5), 0.0),
+                                  origin=(0.0, 0.01 * r, 0.0)), p)
+        w.finalize()
+        offs = np.array([i.point_offset for i in w.rod_infos])
+        w.point_locked[offs] = True
+        w.inv_masses[offs] = 0.0
+        w.static_version += 1
+        return w
+    g, r = make(), make()
+    plan = run_gpu(g, 40, 8)
+    # materials differ between rods: never launch-uniform; one rod per stream
+    # task is CTA-uniform (UNI = 1), packed CTAs mix them (UNI = 0)
+    assert plan["groups"][0]["tier"] == tier
+    assert plan["groups"][0]["uniform"] == (True if tier == "stream" else False)
+    OracleStepper(r).run(40)
+    assert_bitwise(g, r)
