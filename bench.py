@@ -267,19 +267,29 @@ def cpu_single_rod_us(make, steps):
 # ---- distributed plumbing ---------------------------------------------------
 
 def dist_env():
-    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
-            int(os.environ.get("LOCAL_RANK", "0")))
+    """(world size, rank, device).  RSB_BENCH_DEVICE pins every rank to one
+    device -- with RSB_BENCH_DIST=gloo that runs the multi-rank code path on
+    a one-GPU box (a test of the sharding / max-over-ranks / gather logic,
+    never a scaling number)."""
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "RSB_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["RSB_BENCH_DEVICE"])
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), local)
 
 
 class Dist:
     def __init__(self, world, rank, local):
         self.world, self.rank, self.local = world, rank, local
         self.pg = None
+        self.backend = os.environ.get("RSB_BENCH_DIST", "nccl")
         if world > 1:
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group(self.backend)
             self.dist = dist
             self.torch = torch
             self.pg = True
@@ -291,7 +301,7 @@ class Dist:
     def max(self, x):
         if not self.pg:
             return x
-        t = self.torch.tensor([float(x)], device="cuda")
+        t = self.torch.tensor([float(x)], device="cuda" if self.backend == "nccl" else "cpu")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -534,7 +544,9 @@ def run_ours(args):
         ptr = dev.device_ptr(0)
         src = torch.as_tensor(_CudaArray(ptr, (P * 3,), "<f8" if real == 8 else "<f4"),
                               device=f"cuda:{local}")
-        out = torch.empty(world * P * 3, dtype=src.dtype, device=f"cuda:{local}")
+        if D.backend != "nccl":   # gloo test path: gather through host memory
+            src = src.cpu()
+        out = torch.empty(world * P * 3, dtype=src.dtype, device=src.device)
         D.dist.all_gather_into_tensor(out, src.contiguous())
         torch.cuda.synchronize()
         gathered = int(out.numel())
