@@ -59,6 +59,8 @@ enum rs_precision {
 #define RS_STATE   0x1u     /* positions, velocities, frames, angular velocities */
 #define RS_STATIC  0x2u     /* material arrays, masses, locks, bindings, maps */
 #define RS_CONTROL 0x4u     /* drivers and grab anchors */
+#define RS_STATIC_IF_CHANGED 0x8u  /* RS_STATIC only if a static array differs
+                                      from the last static upload (memcmp) */
 
 /* Host view of a World (world.py:77-182).  All arrays are C-contiguous,
  * float64 / int64 / uint8 exactly as the reference World holds them, and

@@ -30,6 +30,7 @@ PRECISIONS = {"f64": RS_F64_MIRROR, "f32": RS_F32, "f64_fast": RS_F64_FAST}
 RS_STATE = 0x1
 RS_STATIC = 0x2
 RS_CONTROL = 0x4
+RS_STATIC_IF_CHANGED = 0x8
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32

@@ -175,6 +175,7 @@ struct rs_handle_s {
                                     // kernel drains the ring at every step
     DevBuf g_act_d, g_pt_d, g_tgt_d;   // world grab slots on the device (live)
     bool control_dirty = false;
+    std::vector<char> static_snap;  // static arrays at the last RS_STATIC upload
     // last uploaded controls (upload_control skips unchanged ones)
     bool ctl_valid = false;
     std::vector<double> ctl_drv_v, ctl_drv_rot, ctl_g_tgt;
@@ -796,11 +797,46 @@ bool contacts_needed(const rs_world_desc& d) {
     return on;
 }
 
+// The static arrays' bytes, in a fixed order: what RS_STATIC_IF_CHANGED
+// compares against the last static upload (the reference reads these arrays
+// live every step, so an in-place edit must take effect at the next epoch).
+std::vector<std::pair<const void*, size_t>> static_spans(const rs_world_desc& d) {
+    const size_t P = size_t(d.P), E = size_t(d.E), R = size_t(d.R), f = sizeof(double), i = sizeof(int64_t);
+    return {{d.rest, E * f},        {d.ustar, 3 * E * f},    {d.mass, P * f},       {d.invm, P * f},
+            {d.inert, 3 * E * f},   {d.fext, 3 * P * f},     {d.ks, E * f},         {d.kp, E * f},
+            {d.gt, E * f},          {d.gr, E * f},           {d.ext, E * f},        {d.kb, 3 * E * f},
+            {d.plock, P},           {d.flock, E},            {d.jvalid, E},         {d.elem_point, E * i},
+            {d.elem_parity, E * i}, {d.drv_pt, R * i},       {d.drv_fr, R * i},     {d.bind_a, size_t(d.nbind) * i},
+            {d.bind_b, size_t(d.nbind) * i}, {d.bind_mode, size_t(d.nbind) * i}, {d.cradii, P * f},
+            {d.cmask, P}};
+}
+
+void snapshot_static(rs_handle h) {
+    h->static_snap.clear();
+    for (auto& sp : static_spans(h->d)) {
+        const char* p = static_cast<const char*>(sp.first);
+        if (p) h->static_snap.insert(h->static_snap.end(), p, p + sp.second);
+    }
+}
+
+bool static_changed(rs_handle h) {
+    size_t off = 0;
+    for (auto& sp : static_spans(h->d)) {
+        if (!sp.first) continue;
+        if (off + sp.second > h->static_snap.size() ||
+            std::memcmp(h->static_snap.data() + off, sp.first, sp.second) != 0)
+            return true;
+        off += sp.second;
+    }
+    return off != h->static_snap.size();
+}
+
 int upload_static(rs_handle h) {
     const rs_world_desc& d = h->d;
     std::vector<uint32_t> pflags;
     std::vector<int32_t> pt_elem;
     h->contacts_on = contacts_needed(d);
+    snapshot_static(h);
     int rc = plan(h, pflags, pt_elem);
     if (rc) return rc;
     const size_t P = size_t(d.P), E = size_t(d.E), R = size_t(d.R);
@@ -1101,7 +1137,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
 }
 
 void register_host(rs_handle h, void* p, size_t bytes) {
-    if (!p || bytes < (size_t(1) << 20)) return;
+    if (!p || bytes == 0) return;   // page-locked: async copies, no staging
     if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess)
         h->registered.push_back(p);
     else
@@ -1283,7 +1319,7 @@ int rs_upload(rs_handle h, uint32_t mask) {
         if ((rc = upload_control(h))) return rc;
         h->control_dirty = false;
     }
-    if (mask & RS_STATIC) {
+    if ((mask & RS_STATIC) || ((mask & RS_STATIC_IF_CHANGED) && static_changed(h))) {
         CK(cudaStreamSynchronize(h->st));
         if ((rc = upload_static(h))) return rc;
     }

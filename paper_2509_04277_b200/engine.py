@@ -206,8 +206,6 @@ class Engine:
         self._bound_scene = self._scene_key()
         self._static_version = self.world.static_version
         self._small = self.world.num_points <= SMALL_WORLD_POINTS
-        self._static_copy = ({a: np.array(getattr(self.world, a), copy=True)
-                              for a in _STATIC_ATTRS} if self._small else None)
 
     def _scene_key(self):
         w = self.world
@@ -224,17 +222,14 @@ class Engine:
             # an array attribute was replaced: re-bind (re-plans and uploads)
             self._bind()
             return False
-        static_dirty = w.static_version != self._static_version
-        if self._small and not static_dirty:
-            static_dirty = any(not np.array_equal(getattr(w, a), c)
-                               for a, c in self._static_copy.items())
         mask = (_lib.RS_STATE if state else 0) | _lib.RS_CONTROL
-        if static_dirty:
+        if w.static_version != self._static_version:
             mask |= _lib.RS_STATIC
             self._static_version = w.static_version
-            if self._small:
-                self._static_copy = {a: np.array(getattr(w, a), copy=True)
-                                     for a in _STATIC_ATTRS}
+        elif self._small:
+            # the reference reads the static arrays live: catch in-place
+            # edits (a memcmp against the last upload, in the library)
+            mask |= _lib.RS_STATIC_IF_CHANGED
         self._dev.upload(mask)
         return True
 
