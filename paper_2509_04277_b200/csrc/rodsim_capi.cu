@@ -1189,7 +1189,24 @@ constexpr int kPipeChunks = 16;
 int run_epoch_pipelined(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
     const Group& g = h->groups[0];
     const rs_world_desc& d = h->d;
-    const int C = std::min(g.ncta, kPipeChunks);
+    // chunk boundaries: equal chunks in the middle, the first and last ones
+    // ramped down (1/8, 1/4, 1/2 of a chunk), so the pipeline's fill (H2D of
+    // the first chunk alone) and drain (D2H of the last alone) are short
+    std::vector<double> w;
+    for (double f : {0.125, 0.25, 0.5}) w.push_back(f);
+    for (int i = 0; i < kPipeChunks - 6; ++i) w.push_back(1.0);
+    for (double f : {0.5, 0.25, 0.125}) w.push_back(f);
+    double wsum = 0;
+    for (double x : w) wsum += x;
+    std::vector<int> cut{0};
+    double acc = 0;
+    for (double x : w) {
+        acc += x;
+        const int t = int(std::llround(double(g.ncta) * acc / wsum));
+        if (t > cut.back()) cut.push_back(std::min(t, g.ncta));
+    }
+    if (cut.back() != g.ncta) cut.push_back(g.ncta);
+    const int C = int(cut.size()) - 1;
     if (!h->st_in) {
         CK(cudaStreamCreateWithFlags(&h->st_in, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&h->st_out, cudaStreamNonBlocking));
@@ -1210,7 +1227,7 @@ int run_epoch_pipelined(rs_handle h, int64_t steps, int64_t* contacts, int64_t* 
     DevBuf* const dp[4] = {&h->pos, &h->vel, &h->q, &h->w};
     const int width[4] = {3, 3, 4, 3};
     for (int c = 0; c < C; ++c) {
-        const int t0 = int(int64_t(g.ncta) * c / C), t1 = int(int64_t(g.ncta) * (c + 1) / C);
+        const int t0 = cut[c], t1 = cut[c + 1];
         const CtaTask& a = h->h_tasks[g.task_begin + t0];
         const CtaTask& b = h->h_tasks[g.task_begin + t1 - 1];
         const int64_t P0 = a.p0, P1 = int64_t(b.p0) + b.np;

@@ -322,15 +322,17 @@ class Engine:
         return self._dev.stage_commands(ops)
 
     def _resolve_applied(self):
-        still = []
-        for cmd, ticket, slot in self._pending:
-            step = self._dev.applied_step_for(slot)
-            if step >= 0:
-                self.command_log.append((step, cmd))
-                ticket.resolve(step)
-            else:
-                still.append((cmd, ticket, slot))
-        self._pending = still
+        # _stage_pending may append from a posting thread meanwhile
+        with self._stage_lock:
+            still = []
+            for cmd, ticket, slot in self._pending:
+                step = self._dev.applied_step_for(slot)
+                if step >= 0:
+                    self.command_log.append((step, cmd))
+                    ticket.resolve(step)
+                else:
+                    still.append((cmd, ticket, slot))
+            self._pending = still
 
     # -- stepping ----------------------------------------------------------
 
