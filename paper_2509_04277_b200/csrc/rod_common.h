@@ -123,6 +123,7 @@ struct StepArgs {
     unsigned long long *prof;                      // (PROF_SLOTS) phase cycle sums
     int32_t any_binds;                             // launch has bindings (cluster/grid:
     int32_t any_grabs;                             //   barrier count must be uniform)
+    int32_t any_dist;                              // launch has distance-projected elements
     int32_t ntasks;                                // stream tier: tasks for gridDim CTAs
     Real dt, beta, gx, gy, gz;
     UniConsts<Real> u;                             // UNI == 2 launches

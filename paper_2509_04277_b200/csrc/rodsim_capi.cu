@@ -99,6 +99,7 @@ struct Group {       // one kernel launch
     int tier = TIER_CTA;
     int variant = 0;
     int uni = 0;                    // constants: 0 per slot, 1 per CTA, 2 per launch
+    bool any_dist = true;           // some element of the launch is distance-projected
     int32_t e_launch = 0;           // element standing for the launch (uni == 2)
     int task_begin = 0, ncta = 0;   // tasks (one CTA each, except stream)
     int grid = 0;                   // CTAs launched (stream: persistent)
@@ -655,6 +656,13 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             }
         }
         g.uni = uni ? (launch_uni && g_e0 >= 0 ? 2 : 1) : 0;
+        g.any_dist = false;
+        for (int t = g.task_begin; t < g.task_begin + g.ncta && !g.any_dist; ++t)
+            for (int64_t p = h->h_tasks[t].p0; p < h->h_tasks[t].p0 + h->h_tasks[t].np; ++p)
+                if (pflags[p] & SF_DIST) {
+                    g.any_dist = true;
+                    break;
+                }
         g.e_launch = int32_t(std::max<int64_t>(g_e0, 0));
         g.bind_cap = bcap;
         g.drv_cap = std::max(dcap, 1);
@@ -1030,6 +1038,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
         a.any_binds |= h->h_tasks[t].bind_count > 0;
         a.any_grabs |= h->h_tasks[t].grab_count > 0;
     }
+    a.any_dist = g.any_dist;
     if (g.uni == 2) {   // the same arithmetic the kernel's load_elem_consts does
         const int64_t e = g.e_launch;
         const rs_world_desc& d = h->d;
