@@ -158,6 +158,11 @@ int rs_stage_commands(rs_handle h, const double *ops, int64_t n, int64_t *slots)
 int64_t rs_applied_step_for(rs_handle h, int64_t global_slot);
 /* Snapshot of the last completed epoch: pos (P,3), q (E,4). */
 int rs_read_snapshot(rs_handle h, double *pos, double *q, int64_t *seq, int64_t *step);
+/* Live handles: 1 = the kernel publishes a snapshot after every step
+ * (ph_publish, _core.pyx:1045-1052; double-buffered in mapped host memory,
+ * read by rs_read_snapshot while a launch runs); 0 = snapshots at epoch
+ * boundaries only (the default: per-step publishing costs PCIe writes). */
+int rs_live_snapshots(rs_handle h, int on);
 void rs_destroy(rs_handle h);
 const char *rs_last_error(void);
 

@@ -102,6 +102,7 @@ SIGNATURES = [
     ("rs_pipe_peak", _i32, [_i32, ctypes.POINTER(_f64)]),
     ("rs_plan_dry", _i32, [ctypes.POINTER(WorldDesc), _i32, ctypes.c_char_p, _i64]),
     ("rs_micro", _i32, [_i32, _i32, ctypes.POINTER(_f64)]),
+    ("rs_live_snapshots", _i32, [_p, _i32]),
 ]
 
 MICRO_KINDS = {"dadd": 0, "dmul": 1, "dfma": 2, "div": 3, "sqrt_add": 4, "div_rn": 5,
@@ -338,6 +339,9 @@ class DeviceWorld:
 
     def applied_step_for(self, slot):
         return int(self.lib.rs_applied_step_for(self.handle, int(slot)))
+
+    def live_snapshots(self, on=True):
+        check(self.lib.rs_live_snapshots(self.handle, 1 if on else 0), self.lib)
 
     def read_snapshot(self):
         w = self.world

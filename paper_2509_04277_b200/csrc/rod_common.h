@@ -94,6 +94,17 @@ struct LiveRing {
     double rows[RING_CAP][6];       // [op, i0, i1, f0, f1, f2]
 };
 
+// Per-step snapshot of a live launch (ph_publish, _core.pyx:1045-1052), in
+// mapped host memory: two position/frame buffers; the step after which each
+// was written; `pub` = version, the readable buffer being version & 1.  The
+// kernel writes the other buffer during step s and flips `pub` (release,
+// system scope) after the barrier that ends it; a reader copies the buffer
+// and retries if `pub` moved meanwhile.
+struct LiveSnap {
+    int64_t pub;
+    int64_t step[2];
+};
+
 // Kernel arguments; device pointers, AoS layouts identical to world.py.
 template <typename Real>
 struct StepArgs {
@@ -152,6 +163,9 @@ struct StepArgs {
     int32_t *g_act, *g_pt;                         // (ngrab) world grab slots
     Real* g_tgt;                                   // (ngrab,3)
     int32_t ngrab, nrods;
+    LiveSnap* snap;                                // live per-step snapshot (or null)
+    double *snap_pos, *snap_q;                     // (2, P, 3), (2, E, 4)
+    int64_t snap_base, snap_P, snap_E;             // version at launch start, sizes
 };
 
 constexpr int PROF_SLOTS = 64;

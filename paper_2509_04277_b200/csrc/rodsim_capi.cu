@@ -175,6 +175,12 @@ struct rs_handle_s {
     bool live = false;              // the plan is one CTA / one cluster: the
                                     // kernel drains the ring at every step
     DevBuf g_act_d, g_pt_d, g_tgt_d;   // world grab slots on the device (live)
+    LiveSnap* snap = nullptr;          // live per-step snapshot, mapped host memory
+    LiveSnap* snap_dev = nullptr;
+    double *snap_pos = nullptr, *snap_q = nullptr;         // (2,P,3), (2,E,4) mapped
+    double *snap_pos_dev = nullptr, *snap_q_dev = nullptr;
+    int64_t snap_version = 0;          // published snapshot version (host view)
+    bool snap_on = false;              // per-step snapshots requested (rs_live_snapshots)
     bool control_dirty = false;
     std::vector<char> static_snap;  // static arrays at the last RS_STATIC upload
     // last uploaded controls (upload_control skips unchanged ones)
@@ -1089,6 +1095,12 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.pair_acc = static_cast<Real*>(h->pair_acc.p);
     a.pair_count = h->d_pairs;
     a.live = h->live ? h->ring_dev : nullptr;
+    a.snap = (h->live && h->snap_on) ? h->snap_dev : nullptr;
+    a.snap_pos = h->snap_pos_dev;
+    a.snap_q = h->snap_q_dev;
+    a.snap_base = h->snap_version;
+    a.snap_P = h->d.P;
+    a.snap_E = h->d.E;
     a.drv_v_live = static_cast<Real*>(h->drv_v.p);
     a.drv_rot_live = static_cast<Real*>(h->drv_rot.p);
     a.g_act = static_cast<int32_t*>(h->g_act_d.p);
@@ -1299,6 +1311,26 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     }
     std::memset(h->ring, 0, sizeof(LiveRing));
     for (int i = 0; i < RING_CAP; ++i) h->ring->apply[i] = -1;
+    if (desc->live) {   // per-step snapshot buffers of live launches
+        const size_t P = size_t(desc->P), E = size_t(desc->E);
+        auto mapped = [&](void** hp, void** dp, size_t bytes) {
+            return cudaHostAlloc(hp, bytes, cudaHostAllocMapped) == cudaSuccess &&
+                   cudaHostGetDevicePointer(dp, *hp, 0) == cudaSuccess;
+        };
+        if (!mapped(reinterpret_cast<void**>(&h->snap), reinterpret_cast<void**>(&h->snap_dev), sizeof(LiveSnap)) ||
+            !mapped(reinterpret_cast<void**>(&h->snap_pos), reinterpret_cast<void**>(&h->snap_pos_dev),
+                    2 * 3 * P * sizeof(double)) ||
+            !mapped(reinterpret_cast<void**>(&h->snap_q), reinterpret_cast<void**>(&h->snap_q_dev),
+                    2 * 4 * E * sizeof(double))) {
+            cudaGetLastError();
+            rs_destroy(h);
+            return fail(RS_E_CUDA, "mapped snapshot allocation failed");
+        }
+        std::memcpy(h->snap_pos, desc->pos, 3 * P * sizeof(double));   // version 0: the bound state
+        std::memcpy(h->snap_q, desc->q, 4 * E * sizeof(double));
+        h->snap->pub = 0;
+        h->snap->step[0] = h->snap->step[1] = desc->step_index;
+    }
     int rc = RS_OK;
     auto bail = [&](int code) {
         rs_destroy(h);
@@ -1370,6 +1402,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
             int rc = launch_group(h, g, h->step + done, k);
             if (rc) return rc;
         }
+        if (h->live && h->snap && h->snap_on) h->snap_version += k;   // one snapshot per step
         done += k;
     }
     h->prof_steps += steps;
@@ -1513,8 +1546,41 @@ int64_t rs_applied_step_for(rs_handle h, int64_t global_slot) {
     return R->apply[global_slot % RING_CAP];
 }
 
+int rs_live_snapshots(rs_handle h, int on) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    if (on && !h->snap) return fail(RS_E_INVALID, "per-step snapshots need a live handle (desc.live = 1)");
+    if (on && !h->snap_on) {   // the last published buffer must hold the current state
+        CK(cudaStreamSynchronize(h->st));
+        const int b = int(h->snap_version & 1);
+        std::memcpy(h->snap_pos + size_t(b) * 3 * size_t(h->d.P), h->d.pos, sizeof(double) * 3 * size_t(h->d.P));
+        std::memcpy(h->snap_q + size_t(b) * 4 * size_t(h->d.E), h->d.q, sizeof(double) * 4 * size_t(h->d.E));
+        h->snap->step[b] = h->step;
+        h->snap->pub = h->snap_version;
+    }
+    h->snap_on = on != 0;
+    return RS_OK;
+}
+
 int rs_read_snapshot(rs_handle h, double* pos, double* q, int64_t* seq, int64_t* step) {
     if (!h) return fail(RS_E_INVALID, "null handle");
+    if (h->live && h->snap && h->snap_on) {   // the kernel publishes one per step (ph_publish)
+        volatile LiveSnap* S = h->snap;
+        for (int tries = 0; tries < (1 << 20); ++tries) {
+            const int64_t v1 = S->pub;
+            std::atomic_thread_fence(std::memory_order_acquire);
+            const int b = int(v1 & 1);
+            if (pos) std::memcpy(pos, h->snap_pos + size_t(b) * 3 * size_t(h->d.P), sizeof(double) * 3 * size_t(h->d.P));
+            if (q) std::memcpy(q, h->snap_q + size_t(b) * 4 * size_t(h->d.E), sizeof(double) * 4 * size_t(h->d.E));
+            const int64_t st = S->step[b];
+            std::atomic_thread_fence(std::memory_order_acquire);
+            if (S->pub == v1) {
+                if (seq) *seq = 2 * v1;
+                if (step) *step = st;
+                return RS_OK;
+            }
+        }
+        return fail(RS_E_RUNTIME, "snapshot read kept tearing");
+    }
     // the host arrays hold the state of the last completed download
     if (pos) std::memcpy(pos, h->d.pos, sizeof(double) * 3 * size_t(h->d.P));
     if (q) std::memcpy(q, h->d.q, sizeof(double) * 4 * size_t(h->d.E));
@@ -1560,6 +1626,9 @@ void rs_destroy(rs_handle h) {
     if (h->h_contacts) cudaFreeHost(h->h_contacts);
     if (h->stage) cudaFreeHost(h->stage);
     if (h->ring) cudaFreeHost(h->ring);
+    if (h->snap) cudaFreeHost(h->snap);
+    if (h->snap_pos) cudaFreeHost(h->snap_pos);
+    if (h->snap_q) cudaFreeHost(h->snap_q);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->tm0) cudaEventDestroy(h->tm0);

@@ -185,6 +185,7 @@ class Engine:
         self._stage_lock = threading.Lock()
         self._running = False      # an epoch's launch is in flight
         self._live = False
+        self._live_snaps = False   # per-step snapshots requested
         self._snapshot_readers = False
         self._snapshot_stale = False
         self._dev = None
@@ -201,6 +202,7 @@ class Engine:
                                      force_tier=ft, force_ctas=fc,
                                      force_variant=fv, live=self._want_live)
         self._live = bool(self._dev.plan().get("live", False))
+        self._live_snaps = False
         self._bound = {a: getattr(self.world, a) for a in _BOUND_ATTRS}
         # the mesh and the collision scalars are bound too (make_context)
         self._bound_scene = self._scene_key()
@@ -387,6 +389,17 @@ class Engine:
         self._dev.update_params(self.world.dt, self.world.solver.iterations)
 
     def read_snapshot(self):
+        """The latest published (positions, frames).  Live engines read the
+        kernel's per-step snapshot, so a reader sees progress inside a
+        running epoch (ph_publish, _core.pyx:1045-1052); otherwise the
+        snapshot is published at epoch boundaries."""
+        if self._live:
+            if not self._live_snaps:   # from the next launch on, one per step
+                with self._lock:
+                    self._dev.live_snapshots(True)
+                    self._live_snaps = True
+            seq, step, pos, frames = self._dev.read_snapshot()
+            return Snapshot(seq, step, pos, frames)
         with self._lock:
             self._snapshot_readers = True
             if self._snapshot_stale:

@@ -95,3 +95,32 @@ def test_live_is_opt_in():
         assert not eng.plan()["live"]
     with Engine(wl.cantilever(), backend="parallel") as eng:
         assert eng.plan()["live"]
+
+
+def test_live_snapshots_during_an_epoch_match_the_oracle():
+    # per-step snapshots published by the kernel (ph_publish): read while a
+    # long epoch runs, each equals the oracle's state at its step, bit for bit
+    steps = 3000
+    g = wl.pair()
+    snaps = []
+    with Engine(g, live=True) as eng:
+        eng.read_snapshot()                   # a reader: per-step publishing on
+        eng.run_epoch(1)
+        th = threading.Thread(target=lambda: eng.run_epoch(steps))
+        th.start()
+        while th.is_alive() and len(snaps) < 40:
+            snaps.append(eng.read_snapshot())
+            time.sleep(0.001)
+        th.join()
+        last = eng.read_snapshot()
+    assert last.step_index == 1 + steps
+    assert np.array_equal(_bits(last.positions), _bits(g.positions))
+    mid = [s for s in snaps if 1 < s.step_index < 1 + steps]
+    assert len(mid) >= 3
+    assert all(a.step_index <= b.step_index for a, b in zip(snaps, snaps[1:]))
+    r = wl.pair()
+    o = OracleStepper(r)
+    for s in sorted({s.step_index: s for s in mid}.values(), key=lambda s: s.step_index):
+        o.run(s.step_index - r.step_index)
+        assert np.array_equal(_bits(s.positions), _bits(r.positions)), s.step_index
+        assert np.array_equal(_bits(s.frames), _bits(r.frames)), s.step_index

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--force-variant", type=int, default=-1)
     ap.add_argument("--force-tier", type=int, default=-1)
     ap.add_argument("--force-ctas", type=int, default=0)
+    ap.add_argument("--live", action="store_true")
     a = ap.parse_args()
     if a.case == "hair":
         w = wl.hair(a.rods)
@@ -35,7 +36,7 @@ def main():
         w = wl.sweep(a.n)
     else:
         w = getattr(wl, a.case)()
-    kw = dict(precision=a.precision, force_variant=a.force_variant)
+    kw = dict(precision=a.precision, force_variant=a.force_variant, live=a.live)
     if a.force_tier >= 0:
         kw["force_tier"] = a.force_tier
     if a.force_ctas:
