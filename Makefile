@@ -3,7 +3,10 @@
 #   make ref        -> oracle/_ref (the reference's own compiled core, if present)
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v
+# PROF=1 compiles in the per-phase cycle profile (RSB_DEBUG=2 at run time;
+# rebuild from clean when toggling)
+PROF    ?= 0
+NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v -DRSB_PROF=$(PROF)
 CSRC    := paper_2509_04277_b200/csrc
 LIB     := paper_2509_04277_b200/librodsim_b200.so
 HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/rodsim_b200.h
