@@ -369,3 +369,46 @@ def test_mixed_batch_bitwise(lo, tier):
     assert plan["groups"][0]["uniform"] == (True if tier == "stream" else False)
     OracleStepper(r).run(40)
     assert_bitwise(g, r)
+
+
+# -- dividends outside the fast-division window --------------------------------
+# Straight rods with exactly representable geometry (spacing 0.125, identity
+# frames, no gravity) have zero position bias, so with velocities ~1e-200
+# nearly every quotient of the step has a dividend below 2^-400 and takes
+# the IEEE fallback of div_rn (rod_math.cuh) -- including the vote-gated one
+# of the branch-free colour phase.  Tiny and normal rods alternate, so one
+# warp holds lanes on both paths.
+
+def _tiny_world(nrods, npts, tiny_every=2, scale=1e-200, seed=3):
+    w = World(dt=1e-4, gravity=(0.0, 0.0, 0.0))
+    for r in range(nrods):
+        w.add_rod(st.init_rod(npts, 0.125 * (npts - 1), axis=(0.0, 0.0, 1.0),
+                              origin=(float(r), 0.0, 0.0)), st.RodParams())
+    w.finalize()
+    rng = np.random.default_rng(seed)
+    for r, info in enumerate(w.rod_infos):
+        sc = scale if r % tiny_every == 0 else 1e-3
+        p = slice(info.point_offset, info.point_offset + info.num_points)
+        e = slice(info.elem_offset, info.elem_offset + info.num_points - 1)
+        w.velocities[p] = sc * rng.normal(size=(info.num_points, 3))
+        w.angular_velocities[e] = sc * rng.normal(size=(info.num_points - 1, 3))
+    return w
+
+
+@pytest.mark.parametrize("nrods,npts,kw", [
+    (1, 16, {}),                                  # one rod, one warp
+    (40, 9, {}),                                  # rods packed per CTA: mixed lanes
+    (1, 200, {"force_tier": 1, "force_ctas": 3}),  # cluster tier
+])
+def test_tiny_dividends_take_ieee_fallback_bitwise(nrods, npts, kw):
+    g = parity(lambda: _tiny_world(nrods, npts), 20, 7, **kw)
+    assert np.max(np.abs(g.velocities[:npts])) < 1e-150   # stayed in the tiny range
+
+
+@pytest.mark.parametrize("variant", [5, 7])
+def test_tiny_dividends_stream_tier_bitwise(variant):
+    g, r = _tiny_world(330, 129), _tiny_world(330, 129)
+    plan = run_gpu(g, 6, 3, force_variant=variant)
+    assert plan["groups"][0]["tier"] == "stream"
+    OracleStepper(r).run(6)
+    assert_bitwise(g, r)
