@@ -75,9 +75,11 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-# fp64 pipe instructions the fp64 mirror kernel issues per slot-step (ncu SASS
-# count, DADD + DMUL + DFMA, profiles/r01_ncu_*): the compute cross-check
-FP64_INST_PER_SLOT_STEP = 715
+# fp64 pipe instructions the fp64 mirror kernel issues per slot-step (ncu
+# smsp__sass_thread_inst_executed_op_{dadd,dmul,dfma}_pred_on of variant 7,
+# profiles/r01f_ncu_full_hair.json capture: 5.63e9 per launch / 8.45e6
+# slots): the compute cross-check
+FP64_INST_PER_SLOT_STEP = 666
 
 
 def fp64_peak():
