@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "rod_step.cuh"
 
 #if !defined(RSB_MODE_NS) || !defined(RSB_MODE_ID) || !defined(RSB_FEAT)
@@ -25,16 +27,39 @@ namespace RSB_MODE_NS {
 // self-collision phases; the feature TUs carry the CTA V0-V2, V4, cluster and
 // grid variants only (the planner keeps such scenes on those).
 
+// The kernel's function attributes, once per kernel and device (two driver
+// calls per launch otherwise -- a haptic frame is one launch): the dynamic
+// shared-memory limit at the opt-in maximum (the limit only gates launches;
+// occupancy follows the size a launch or query passes) and all of the
+// unified L1/shared array as shared memory -- several CTAs (rods) per SM
+// are what hides latency in the batched case.
+constexpr int kMaxDynSmem = 232448;   // 227 KB opt-in per CTA on sm_100
+template <typename Fn>
+static cudaError_t configure_once(Fn fn, std::atomic<bool>* done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             int(cudaSharedmemCarveoutMaxShared));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev].store(true, std::memory_order_release);
+    return cudaSuccess;
+}
+
+template <typename Real, int S, int CAP, int TIER, int UNI>
+static std::atomic<bool>* configured_flags() {
+    static std::atomic<bool> done[64];
+    return done;
+}
+
 template <typename Real, int S, int CAP, int TIER, int UNI>
 static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
                               size_t smem, int cluster, cudaStream_t st) {
     auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    // all of the unified L1/shared array as shared memory: several CTAs
-    // (rods) per SM are what hides latency in the batched case
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             int(cudaSharedmemCarveoutMaxShared));
+    cudaError_t e = configure_once(fn, configured_flags<Real, S, CAP, TIER, UNI>());
     if (e != cudaSuccess) return e;
     if constexpr (TIER == TIER_CLUSTER) {
         if (cluster > 8) {
@@ -66,10 +91,7 @@ static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
 template <typename Real, int S, int CAP, int TIER, int UNI>
 static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out) {
     auto fn = rod_step_kernel<Real, S, CAP, TIER, UNI, RSB_MODE_ID>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             int(cudaSharedmemCarveoutMaxShared));
+    cudaError_t e = configure_once(fn, configured_flags<Real, S, CAP, TIER, UNI>());
     if (e != cudaSuccess) return e;
     if constexpr (TIER == TIER_CLUSTER) {
         if (cluster > 8) {

@@ -225,6 +225,37 @@ int ensure_stage(rs_handle h, size_t bytes) {
 }
 
 // host double array -> device Real array
+// Several copies between the World's host arrays and the device as one
+// driver call (cudaMemcpyBatchAsync, stream-ordered sources): a small world's
+// epoch moves a few arrays each way, and one call per array cost more than
+// the copies.
+struct CopyBatch {
+    void* dst[8];
+    void* src[8];
+    size_t size[8];
+    size_t n = 0;
+    void add(void* d, const void* s, size_t bytes) {
+        if (bytes == 0) return;
+        dst[n] = d;
+        src[n] = const_cast<void*>(s);
+        size[n] = bytes;
+        ++n;
+    }
+};
+
+int flush_batch(rs_handle h, CopyBatch& b) {
+    if (b.n == 1) {
+        CK(cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, h->st));
+    } else if (b.n > 1) {
+        cudaMemcpyAttributes attr = {};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t first = 0, fail_idx = 0;
+        CK(cudaMemcpyBatchAsync(b.dst, b.src, b.size, b.n, &attr, &first, 1, &fail_idx, h->st));
+    }
+    b.n = 0;
+    return RS_OK;
+}
+
 int put_real(rs_handle h, DevBuf& b, const double* src, size_t count) {
     int rc = dev_alloc(b, std::max<size_t>(count, 1) * h->rsz);
     if (rc) return rc;
@@ -951,12 +982,24 @@ int upload_control(rs_handle h) {
 
 int upload_state(rs_handle h) {
     const rs_world_desc& d = h->d;
-    const size_t P = size_t(d.P);
-    int rc = put_real(h, h->pos, d.pos, 3 * P);
-    if (rc) return rc;
-    if ((rc = put_real(h, h->vel, d.vel, 3 * P))) return rc;
-    if ((rc = put_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
-    if ((rc = put_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+    const size_t P = size_t(d.P), E = size_t(d.E);
+    int rc = RS_OK;
+    if (h->rsz == sizeof(double) && d.pos && d.vel && d.q && d.w) {
+        if ((rc = dev_alloc(h->pos, 8 * 3 * std::max<size_t>(P, 1))) || (rc = dev_alloc(h->vel, 8 * 3 * std::max<size_t>(P, 1))) ||
+            (rc = dev_alloc(h->q, 8 * 4 * std::max<size_t>(E, 1))) || (rc = dev_alloc(h->w, 8 * 3 * std::max<size_t>(E, 1))))
+            return rc;
+        CopyBatch b;
+        b.add(h->pos.p, d.pos, 8 * 3 * P);
+        b.add(h->vel.p, d.vel, 8 * 3 * P);
+        b.add(h->q.p, d.q, 8 * 4 * E);
+        b.add(h->w.p, d.w, 8 * 3 * E);
+        if ((rc = flush_batch(h, b))) return rc;
+    } else {
+        if ((rc = put_real(h, h->pos, d.pos, 3 * P))) return rc;
+        if ((rc = put_real(h, h->vel, d.vel, 3 * P))) return rc;
+        if ((rc = put_real(h, h->q, d.q, 4 * E))) return rc;
+        if ((rc = put_real(h, h->w, d.w, 3 * E))) return rc;
+    }
     if (d.has_self) {
         if ((rc = put_i32(h, h->pair_a, d.pair_a, size_t(d.pair_cap)))) return rc;
         if ((rc = put_i32(h, h->pair_b, d.pair_b, size_t(d.pair_cap)))) return rc;
@@ -1455,10 +1498,19 @@ int rs_download(rs_handle h, uint32_t mask) {
     if ((mask & (RS_STATE | RS_CONTROL)) && h->live && h->planned)
         if ((rc = download_control(h))) return rc;
     if (mask & RS_STATE) {
-        if ((rc = get_real(h, h->pos, d.pos, 3 * size_t(d.P)))) return rc;
-        if ((rc = get_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
-        if ((rc = get_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
-        if ((rc = get_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+        if (h->rsz == sizeof(double)) {
+            CopyBatch b;
+            if (d.pos) b.add(d.pos, h->pos.p, 8 * 3 * size_t(d.P));
+            if (d.vel) b.add(d.vel, h->vel.p, 8 * 3 * size_t(d.P));
+            if (d.q) b.add(d.q, h->q.p, 8 * 4 * size_t(d.E));
+            if (d.w) b.add(d.w, h->w.p, 8 * 3 * size_t(d.E));
+            if ((rc = flush_batch(h, b))) return rc;
+        } else {
+            if ((rc = get_real(h, h->pos, d.pos, 3 * size_t(d.P)))) return rc;
+            if ((rc = get_real(h, h->vel, d.vel, 3 * size_t(d.P)))) return rc;
+            if ((rc = get_real(h, h->q, d.q, 4 * size_t(d.E)))) return rc;
+            if ((rc = get_real(h, h->w, d.w, 3 * size_t(d.E)))) return rc;
+        }
         if (d.has_self) {
             const size_t n = size_t(d.pair_cap);
             std::vector<int32_t> ia(n), ib(n);

@@ -36,3 +36,14 @@ with Engine(w) as eng:
     kern = dev.timer_ms() / n / 1e3
     print({"frame_us": frame * 1e6, "push_us": push * 1e6, "run_host_us": run_host * 1e6,
            "device_us": kern * 1e6})
+
+    # pieces of run_epoch on the host side
+    import cProfile
+    import pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    for i in range(300):
+        eng.post_command("insert_velocity", rod=0, value=0.05, axis=(0.0, 0.0, 1.0))
+        eng.run_epoch(10)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(14)
