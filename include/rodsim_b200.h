@@ -176,8 +176,13 @@ double rs_last_kernel_ms(rs_handle h);
 int rs_timer_start(rs_handle h);
 int rs_timer_stop(rs_handle h);
 double rs_timer_ms(rs_handle h);
-/* Number of kernel launches issued so far. */
+/* Number of kernel launches issued so far (a speculative batched step is
+ * two: the speculative kernel and the exact one over its redo list). */
 int64_t rs_launch_count(rs_handle h);
+/* Rods the last speculative batched launch handed to the exact kernel
+ * (quotients outside the fast path's window); 0 when none or when the
+ * handle has no speculative launches.  Synchronises the stream. */
+int64_t rs_last_redo_count(rs_handle h);
 /* JSON description of the launch plan (tiers, CTAs, threads, variants). */
 int rs_plan_json(rs_handle h, char *buf, int64_t len);
 /* The same plan computed without a device (no CUDA calls, no occupancy

@@ -93,6 +93,7 @@ SIGNATURES = [
     ("rs_enable_timing", _i32, [_p, _i32]),
     ("rs_last_kernel_ms", _f64, [_p]),
     ("rs_launch_count", _i64, [_p]),
+    ("rs_last_redo_count", _i64, [_p]),
     ("rs_plan_json", _i32, [_p, ctypes.c_char_p, _i64]),
     ("rs_device_ptr", _i32, [_p, _i32, ctypes.POINTER(_p)]),
     ("rs_selftest_div", _i32, [_p, _p, _i64, _p, _p]),
@@ -360,6 +361,10 @@ class DeviceWorld:
 
     def launch_count(self):
         return int(self.lib.rs_launch_count(self.handle))
+
+    def last_redo_count(self):
+        """Rods the last speculative batched launch left to the exact kernel."""
+        return int(self.lib.rs_last_redo_count(self.handle))
 
     def timer_start(self):
         check(self.lib.rs_timer_start(self.handle), self.lib)

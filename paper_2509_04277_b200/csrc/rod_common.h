@@ -132,6 +132,11 @@ struct StepArgs {
     int32_t debug;                                 // bit 0: poison smem (NaN) first,
                                                    // bit 1: per-phase cycles -> prof
     unsigned long long *prof;                      // (PROF_SLOTS) phase cycle sums
+    // speculative batched launches: rods whose quotients left the fast
+    // path's window are listed here (not written back) and stepped again by
+    // the exact kernel, which then reads its tasks from the list
+    int32_t *redo_list, *redo_count;
+    int redo_mode;                                 // 1: tasks = redo_list[0 .. *redo_count)
     int32_t any_binds;                             // launch has bindings (cluster/grid:
     int32_t any_grabs;                             //   barrier count must be uniform)
     int32_t any_dist;                              // launch has distance-projected elements

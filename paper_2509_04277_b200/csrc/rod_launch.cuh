@@ -139,6 +139,23 @@ static cudaError_t dispatch_uni(int what, int cfg, const StepArgs<Real>* a, int 
     return cudaErrorInvalidValue;
 }
 
+// cfg 6..8: the speculative batched kernel (stream tier, variant 7 only)
+template <typename Real, int S, int CAP, int TIER>
+static cudaError_t dispatch_spec(int what, int cfg, const StepArgs<Real>* a, int ncta, int threads,
+                                 size_t smem, int cluster, cudaStream_t st, int* out) {
+#define RSB_U(C)                                                                                          \
+    case C:                                                                                               \
+        return what == 0 ? launch_one<Real, S, CAP, TIER, 6 + C>(*a, ncta, threads, smem, cluster, st) \
+                         : occupancy_one<Real, S, CAP, TIER, 6 + C>(threads, smem, cluster, out);
+    switch (cfg - 6) {
+        RSB_U(0)
+        RSB_U(1)
+        RSB_U(2)
+    }
+#undef RSB_U
+    return cudaErrorInvalidValue;
+}
+
 template <typename Real>
 static cudaError_t dispatch(int what, int variant, int tier, int uni, const StepArgs<Real>* a,
                             int ncta, int threads, size_t smem, int cluster, cudaStream_t st,
@@ -167,6 +184,8 @@ static cudaError_t dispatch(int what, int variant, int tier, int uni, const Step
             case 7: return RSB_D(2, 136, TIER_CTA);
         }
     } else if (tier == TIER_STREAM) {
+        if (uni >= 6 && variant == 7)
+            return dispatch_spec<Real, 2, 136, TIER_STREAM>(what, uni, a, ncta, threads, smem, cluster, st, out);
         switch (variant) {
             case 5: return RSB_D(1, 130, TIER_STREAM);
             case 6: return RSB_D(2, 130, TIER_STREAM);

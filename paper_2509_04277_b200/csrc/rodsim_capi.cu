@@ -134,6 +134,8 @@ struct rs_handle_s {
     int64_t launches_pipelined = 0;   // epochs run by run_epoch_pipelined
     int num_sms = 0;
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
+    bool spec = true;               // speculative batched launches (RSB_SPEC=0: off)
+    DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
 
     // device mirrors
@@ -763,6 +765,11 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             int per_sm = occ;
             if (const char* e = getenv("RSB_STREAM_CTAS")) per_sm = std::max(1, std::min(occ, atoi(e)));
             g.grid = std::min(g.ncta, per_sm * h->num_sms);
+            if (g.variant == 7 && !h->dry) {   // the speculative launch's redo list
+                int rc2 = dev_alloc(h->redo_list, sizeof(int32_t) * size_t(g.ncta));
+                if (!rc2) rc2 = dev_alloc(h->redo_count, sizeof(int32_t));
+                if (rc2) return rc2;
+            }
         }
         if (g.tier == TIER_GRID) {
             CK(cudaMalloc(&g.d_flags, sizeof(int32_t) * g.ncta));
@@ -1171,32 +1178,46 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     if (g.tier == TIER_GRID) CK(cudaMemsetAsync(g.d_flags, 0, sizeof(int32_t) * g.ncta, h->st));
     const int nt = t_cnt < 0 ? g.ncta : t_cnt;
     const int grid = t_cnt < 0 ? g.grid : (g.tier == TIER_STREAM ? std::min(g.grid, nt) : nt);
-    auto sub = [&](auto& a) {
-        a.tasks += t_off;
-        a.ntasks = nt;
+    const int cfg0 = launch_cfg(h, g);
+    // batched rods (stream tier, variant 7): a speculative launch whose
+    // quotients never take the IEEE fallback, then the exact kernel over the
+    // rods it listed (almost always none: the exact launch finds an empty
+    // list and returns)
+    const bool spec = h->spec && g.tier == TIER_STREAM && g.variant == 7 && cfg0 < 3 && h->redo_count.p;
+    if (spec) CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
+    auto one = [&](int cfg, int redo_mode) -> cudaError_t {
+        auto finish = [&](auto& a) {
+            a.tasks += t_off;
+            a.ntasks = nt;
+            if (spec) {
+                a.redo_list = static_cast<int32_t*>(h->redo_list.p);
+                a.redo_count = static_cast<int32_t*>(h->redo_count.p);
+                a.redo_mode = redo_mode;
+            }
+        };
+        const bool feat = cfg >= 3 && cfg < 6;
+        if (h->prec == RS_F64_MIRROR) {
+            auto a = make_args<double>(h, g, step0, steps);
+            finish(a);
+            return feat ? mirror_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
+                        : mirror::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
+        } else if (h->prec == RS_F32) {
+            auto a = make_args<float>(h, g, step0, steps);
+            finish(a);
+            return feat ? f32_feat::launch_step<float>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
+                        : f32::launch_step<float>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
+        }
+        auto a = make_args<double>(h, g, step0, steps);
+        finish(a);
+        return feat ? f64fast_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
+                    : f64fast::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
     };
-    cudaError_t e;
-    const int cfg = launch_cfg(h, g);
-    if (h->prec == RS_F64_MIRROR) {
-        auto a = make_args<double>(h, g, step0, steps);
-        sub(a);
-        e = cfg >= 3 ? mirror_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
-                     : mirror::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
-    } else if (h->prec == RS_F32) {
-        auto a = make_args<float>(h, g, step0, steps);
-        sub(a);
-        e = cfg >= 3 ? f32_feat::launch_step<float>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
-                     : f32::launch_step<float>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
-    } else {
-        auto a = make_args<double>(h, g, step0, steps);
-        sub(a);
-        e = cfg >= 3 ? f64fast_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
-                     : f64fast::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
-    }
+    cudaError_t e = spec ? one(cfg0 + 6, 0) : one(cfg0, 0);
+    if (e == cudaSuccess && spec) e = one(cfg0, 1);
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
                     g.tier, g.variant, g.ncta, g.threads, g.smem, cudaGetErrorString(e));
-    h->launches += 1;
+    h->launches += spec ? 2 : 1;
     return RS_OK;
 }
 
@@ -1345,6 +1366,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     h->rsz = h->prec == RS_F32 ? sizeof(float) : sizeof(double);
     h->step = desc->step_index;
     if (const char* dbg = getenv("RSB_DEBUG")) h->debug = atoi(dbg);
+    if (const char* sp = getenv("RSB_SPEC")) h->spec = atoi(sp) != 0;
     if (cudaHostAlloc(reinterpret_cast<void**>(&h->ring), sizeof(LiveRing), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->ring_dev), h->ring, 0) != cudaSuccess) {
         cudaGetLastError();
@@ -1651,7 +1673,7 @@ void rs_destroy(rs_handle h) {
                       &h->nstart, &h->ncount, &h->torder, &h->tris, &h->cradii, &h->cmask, &h->cact, &h->cnorm,
                       &h->cdepth, &h->cacc_n, &h->cacc_t, &h->grp_rod, &h->grp_gi, &h->grp_s, &h->grp_e,
                       &h->grp_c, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc, &h->g_act_d, &h->g_pt_d,
-                      &h->g_tgt_d})
+                      &h->g_tgt_d, &h->redo_list, &h->redo_count})
         if (b->p) cudaFree(b->p);
     for (Group& g : h->groups) {
         if (g.d_flags) cudaFree(g.d_flags);
@@ -1706,6 +1728,17 @@ double rs_last_kernel_ms(rs_handle h) {
 }
 
 int64_t rs_launch_count(rs_handle h) { return h ? h->launches : -1; }
+
+int64_t rs_last_redo_count(rs_handle h) {
+    if (!h) return -1;
+    if (!h->redo_count.p) return 0;
+    if (cudaSetDevice(h->d.device) != cudaSuccess) return -1;
+    int32_t n = 0;
+    if (cudaMemcpyAsync(&n, h->redo_count.p, sizeof(n), cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||
+        cudaStreamSynchronize(h->st) != cudaSuccess)
+        return -1;
+    return n;
+}
 
 int rs_timer_start(rs_handle h) {
     if (!h) return fail(RS_E_INVALID, "null handle");

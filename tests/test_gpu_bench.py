@@ -30,7 +30,8 @@ def test_bench_line_contract():
     d = _line(out)
     for k in KEYS:
         assert k in d, k
-    assert d["gpu_launches"] == 5 and d["e2e"]["h2d_bytes_per_step"] > 0
+    # a speculative batched step is two launches (the exact one over the redo list)
+    assert d["gpu_launches"] in (5, 10) and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.5
     assert d["config"]["workload"].startswith("cfg5")
 

@@ -412,3 +412,33 @@ def test_tiny_dividends_stream_tier_bitwise(variant):
     assert plan["groups"][0]["tier"] == "stream"
     OracleStepper(r).run(6)
     assert_bitwise(g, r)
+
+
+def test_speculative_batch_redoes_exactly_the_rods_that_need_it():
+    # variant 7 launches speculatively: the tiny rods (every other one) leave
+    # the fast path's window and are stepped again by the exact kernel; the
+    # ordinary hair batch never needs it
+    # (device-resident launches: a host epoch on a batch is pipelined in
+    # chunks, each its own speculative launch)
+    from paper_2509_04277_b200 import _lib
+    g, r = _tiny_world(330, 129), _tiny_world(330, 129)
+    with Engine(g, force_variant=7) as eng:
+        dev = eng.device_world
+        dev.run(3)
+        redone = dev.last_redo_count()
+        dev.run(3)
+        dev.download(_lib.RS_STATE)
+    OracleStepper(r).run(6)
+    assert_bitwise(g, r)
+    assert redone == 165
+    # an ordinary batch: only rods with an exactly zero impulse dividend
+    # (a rod at rest) need it -- a few at the first steps
+    h, hr = wl.hair(1700), wl.hair(1700)
+    with Engine(h) as eng:
+        assert eng.plan()["groups"][0]["variant"] == 7
+        dev = eng.device_world
+        dev.run(2)
+        assert dev.last_redo_count() < 0.02 * 1700
+        dev.download(_lib.RS_STATE)
+    OracleStepper(hr).run(2)
+    assert_bitwise(h, hr)
