@@ -507,8 +507,11 @@ def run_ours(args):
     elem_steps = args.rods * ELEMENTS * args.k * args.steps
     value = elem_steps / (ms_max * 1e-3)
 
-    # roofline: dominant (only) kernel, algorithmic bytes per launch
-    launch_ms = ms / max(launches, 1)
+    # roofline: algorithmic bytes of one step over the time of one step --
+    # the speculative launch plus the exact launch over its redo list (empty
+    # after the first step from rest; a few microseconds), so per step, not
+    # per launch
+    launch_ms = ms / max(args.steps, 1)
     bytes_per_launch = per * algorithmic_bytes_per_rod(ELEMENTS + 1, ELEMENTS, real)
     peak, peak_src = load_peaks()
     achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
@@ -580,7 +583,8 @@ def run_ours(args):
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,
                          "bytes_per_launch": bytes_per_launch,
-                         "launch_ms": launch_ms},
+                         "launch_ms": launch_ms,
+                         "launches_per_step": launches / max(args.steps, 1)},
             "compute_roofline": compute_roofline(per, launch_ms, args.precision),
             "value_k10": value_k10,
             "gpu_launches": launches,
