@@ -171,6 +171,7 @@ struct rs_handle_s {
     // counters, ring, snapshot
     int64_t step = 0;
     int64_t err_step = -1;
+    bool err_pending = false;       // d_err changed since the last read-back
     std::mutex ring_mu;
     LiveRing* ring = nullptr;       // page-locked, device-mapped (rod_common.h)
     LiveRing* ring_dev = nullptr;   // its device address
@@ -245,14 +246,15 @@ struct CopyBatch {
     }
 };
 
-int flush_batch(rs_handle h, CopyBatch& b) {
+int flush_batch(rs_handle h, CopyBatch& b, cudaStream_t st = nullptr) {
+    if (!st) st = h->st;
     if (b.n == 1) {
-        CK(cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, h->st));
+        CK(cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, st));
     } else if (b.n > 1) {
         cudaMemcpyAttributes attr = {};
         attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
         size_t first = 0, fail_idx = 0;
-        CK(cudaMemcpyBatchAsync(b.dst, b.src, b.size, b.n, &attr, &first, 1, &fail_idx, h->st));
+        CK(cudaMemcpyBatchAsync(b.dst, b.src, b.size, b.n, &attr, &first, 1, &fail_idx, st));
     }
     b.n = 0;
     return RS_OK;
@@ -1246,7 +1248,9 @@ int epoch_prelude(rs_handle h) {
 int epoch_epilogue(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
     if (h->timing) CK(cudaEventRecord(h->ev1, h->st));
     h->timed = h->timing;
-    CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+    // the error stamp (a running maximum on the device) is read back when
+    // someone synchronises, not after every launch
+    h->err_pending = true;
     h->step += steps;
     h->snap_seq += 2 * steps;
     h->snap_step = h->step;
@@ -1317,24 +1321,26 @@ int run_epoch_pipelined(rs_handle h, int64_t steps, int64_t* contacts, int64_t* 
         const CtaTask& b = h->h_tasks[g.task_begin + t1 - 1];
         const int64_t P0 = a.p0, P1 = int64_t(b.p0) + b.np;
         const int64_t E0 = P0 - rod_of(d, P0), E1 = P1 - (rod_of(d, P1 - 1) + 1);
+        CopyBatch up;   // the chunk's four state slices, one driver call
         for (int f = 0; f < 4; ++f) {
             const int64_t r0 = f < 2 ? P0 : E0, r1 = f < 2 ? P1 : E1;
             const size_t off = size_t(r0) * width[f], cnt = size_t(r1 - r0) * width[f];
-            CK(cudaMemcpyAsync(static_cast<double*>(dp[f]->p) + off, hp[f] + off, cnt * sizeof(double),
-                               cudaMemcpyHostToDevice, h->st_in));
+            up.add(static_cast<double*>(dp[f]->p) + off, hp[f] + off, cnt * sizeof(double));
         }
+        if (int rc0 = flush_batch(h, up, h->st_in)) return rc0;
         CK(cudaEventRecord(h->ev_in[c], h->st_in));
         CK(cudaStreamWaitEvent(h->st, h->ev_in[c], 0));
         int rc = launch_group(h, g, h->step, int(steps), t0, t1 - t0);
         if (rc) return rc;
         CK(cudaEventRecord(h->ev_k[c], h->st));
         CK(cudaStreamWaitEvent(h->st_out, h->ev_k[c], 0));
+        CopyBatch down;
         for (int f = 0; f < 4; ++f) {
             const int64_t r0 = f < 2 ? P0 : E0, r1 = f < 2 ? P1 : E1;
             const size_t off = size_t(r0) * width[f], cnt = size_t(r1 - r0) * width[f];
-            CK(cudaMemcpyAsync(hp[f] + off, static_cast<const double*>(dp[f]->p) + off, cnt * sizeof(double),
-                               cudaMemcpyDeviceToHost, h->st_out));
+            down.add(hp[f] + off, static_cast<const double*>(dp[f]->p) + off, cnt * sizeof(double));
         }
+        if (int rc1 = flush_batch(h, down, h->st_out)) return rc1;
     }
     int rc = epoch_epilogue(h, steps, contacts, barrier_ns);
     if (rc) return rc;
@@ -1477,6 +1483,10 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
 int rs_synchronize(rs_handle h) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     CK(cudaSetDevice(h->d.device));
+    if (h->err_pending) {
+        CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        h->err_pending = false;
+    }
     CK(cudaStreamSynchronize(h->st));
     if (*h->h_err) h->err_step = std::max<int64_t>(h->err_step, int64_t(*h->h_err) - 1);
     if (h->timed) {
