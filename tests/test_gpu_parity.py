@@ -338,6 +338,34 @@ def test_fp64_fast_mode_within_1e9():
     assert rel <= 1e-9, rel
 
 
+@pytest.mark.parametrize("precision", ["f32", "f64_fast"])
+def test_batched_stream_tier_reduced_precision(precision, monkeypatch):
+    # the speculative batched launches in the fp32 and fast fp64 modes give
+    # the same bits as the exact kernel (RSB_SPEC=0), and stay near the
+    # oracle: fast fp64 within 1e-9 relative; fp32 within 1e-3 L at every
+    # point after 200 steps (1700 randomly oriented rods: a few are
+    # sensitive enough that fp32 drifts past the 1e-5 L stated for the
+    # 8-rod sample, with or without speculation) and 1e-4 L for 99.9 %
+    runs = {}
+    for spec in ("1", "0"):
+        monkeypatch.setenv("RSB_SPEC", spec)
+        g = wl.hair(1700)
+        plan = run_gpu(g, 200, 50, precision=precision)
+        assert plan["groups"][0]["tier"] == "stream" and plan["groups"][0]["variant"] == 7
+        runs[spec] = g
+    for a in ("positions", "velocities", "frames", "angular_velocities"):
+        assert np.array_equal(getattr(runs["1"], a).view(np.int64), getattr(runs["0"], a).view(np.int64)), a
+    r = wl.hair(1700)
+    OracleStepper(r).run(200)
+    g = runs["1"]
+    dr = np.abs(g.positions - r.positions).max(axis=1)
+    if precision == "f64_fast":
+        assert dr.max() <= 1e-9 * np.abs(r.positions).max()
+    else:
+        L = 128 * float(np.mean(r.rest_lengths))
+        assert dr.max() <= 1e-3 * L and np.quantile(dr, 0.999) <= 1e-4 * L
+
+
 @pytest.mark.parametrize("lo,tier", [(66, "stream"), (2, "cta")])
 def test_mixed_batch_bitwise(lo, tier):
     # 1500 rods of lo..129 points, every 7th extensible, bending stiffness
