@@ -86,6 +86,14 @@ constexpr int kBatchVariant = 7;   // batches of short rods; 5 and 6 on request
 // cluster barrier (~300 ns) costs more than the single CTA's extra work.
 constexpr int kClusterVariants[] = {0, 1, 2, 4};
 constexpr int kCtaMaxPoints = 513;   // variant 2 covers 512 slots + the tail
+// A rod without distance-projected elements steps in 3 phases (no colour
+// sweeps), so its one CTA is bound by that SM's fp64 issue rather than by
+// barriers, and a cluster pays from ~320 points on (extensible rods, K = 10:
+// 384 points 4.88 -> 4.52 us/step, 512: 5.69 -> 4.70; 256: 3.77 vs 4.11,
+// tools/ext_sweep.py).  Applied to worlds of a few rods only -- a batch
+// keeps one rod per CTA.
+constexpr int kCtaMaxPointsNoDist = 320;
+constexpr int kFewSegments = 8;
 constexpr int kMaxCluster = 16;
 constexpr int kMaxStepsPerLaunch = 1 << 16;
 constexpr size_t kMaxSmem = 232448;   // 227 KB opt-in per CTA on sm_100
@@ -457,7 +465,14 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     int64_t max_cta_seg = 0;
     for (size_t i = 0; i < segs.size(); ++i) {
         const int64_t np = segs[i].p1 - segs[i].p0;
-        int tier = np <= cta_cap ? TIER_CTA : (np <= int64_t(kMaxCluster) * clu_cap ? TIER_CLUSTER : TIER_GRID);
+        int cap_i = cta_cap;
+        if (d.force_tier < 0 && !d.has_self && !d.has_mesh && segs.size() <= size_t(kFewSegments) &&
+            segs[i].r0 == segs[i].r1) {
+            bool dist = false;
+            for (int64_t p = segs[i].p0; p < segs[i].p1 && !dist; ++p) dist = (pflags[p] & SF_DIST) != 0;
+            if (!dist) cap_i = kCtaMaxPointsNoDist;
+        }
+        int tier = np <= cap_i ? TIER_CTA : (np <= int64_t(kMaxCluster) * clu_cap ? TIER_CLUSTER : TIER_GRID);
         if (d.force_tier >= 0) tier = d.force_tier;
         if (d.has_self && tier != TIER_CTA)
             return fail(RS_E_UNSUPPORTED, "self-collision scenes must fit one CTA (%d points, have %lld)", cta_cap,

@@ -66,7 +66,12 @@ def plan(world, **kw):
 def test_plan_single_rods_by_size():
     g = plan(wl.cantilever())
     assert len(g) == 1 and g[0]["tier"] == "cta" and g[0]["ctas"] == 1 and g[0]["uniform"]
-    assert plan(wl.extensible())[0]["tier"] == "cta"
+    # without distance projection a rod steps in 3 phases: one CTA up to 320
+    # points, a cluster above (the CTA would be bound by one SM's fp64 issue)
+    assert plan(wl.extensible(256))[0]["tier"] == "cta"
+    g = plan(wl.extensible())[0]
+    assert g["tier"] == "cluster" and g["ctas"] >= 2
+    assert plan(wl.cantilever(512))[0]["tier"] == "cta"   # inextensible: 23 phases
     g = plan(wl.sweep(4096))[0]
     assert g["tier"] == "cluster" and 2 <= g["ctas"] <= 16 and g["cluster"] == g["ctas"]
     g = plan(wl.sweep(16384))[0]
