@@ -981,18 +981,26 @@ int upload_control(rs_handle h) {
     auto same = [](const auto& v, const auto* p, size_t n) {
         return v.size() == n && (n == 0 || std::memcmp(v.data(), p, n * sizeof(*p)) == 0);
     };
-    if (h->ctl_valid && h->planned && same(h->ctl_drv_v, d.drv_v, 3 * R) && same(h->ctl_drv_rot, d.drv_rot, R) &&
-        same(h->ctl_g_act, d.g_act, G) && same(h->ctl_g_pt, d.g_pt, G) && same(h->ctl_g_tgt, d.g_tgt, 3 * G))
-        return RS_OK;
-    h->ctl_drv_v.assign(d.drv_v, d.drv_v + 3 * R);
-    h->ctl_drv_rot.assign(d.drv_rot, d.drv_rot + R);
+    // drivers and grabs separately: a haptic frame changes a driver velocity
+    // (two asynchronous copies); the grab slots and tables (copies through
+    // temporaries, with synchronisations) only when a grab changed
+    const bool valid = h->ctl_valid && h->planned;
+    const bool drv_same = valid && same(h->ctl_drv_v, d.drv_v, 3 * R) && same(h->ctl_drv_rot, d.drv_rot, R);
+    const bool grab_same = valid && same(h->ctl_g_act, d.g_act, G) && same(h->ctl_g_pt, d.g_pt, G) &&
+                           same(h->ctl_g_tgt, d.g_tgt, 3 * G);
+    if (drv_same && grab_same) return RS_OK;
+    int rc = RS_OK;
+    if (!drv_same) {
+        h->ctl_drv_v.assign(d.drv_v, d.drv_v + 3 * R);
+        h->ctl_drv_rot.assign(d.drv_rot, d.drv_rot + R);
+        if ((rc = put_real(h, h->drv_v, d.drv_v, 3 * size_t(d.R)))) return rc;
+        if ((rc = put_real(h, h->drv_rot, d.drv_rot, size_t(d.R)))) return rc;
+    }
+    h->ctl_valid = h->planned;
+    if (grab_same) return RS_OK;
     h->ctl_g_act.assign(d.g_act, d.g_act + G);
     h->ctl_g_pt.assign(d.g_pt, d.g_pt + G);
     h->ctl_g_tgt.assign(d.g_tgt, d.g_tgt + 3 * G);
-    h->ctl_valid = h->planned;
-    int rc = put_real(h, h->drv_v, d.drv_v, 3 * size_t(d.R));
-    if (rc) return rc;
-    if ((rc = put_real(h, h->drv_rot, d.drv_rot, size_t(d.R)))) return rc;
     {   // the world's grab slots, as the live kernel drains commands into them
         std::vector<int64_t> act(G);
         for (size_t g = 0; g < G; ++g) act[g] = d.g_act[g];
