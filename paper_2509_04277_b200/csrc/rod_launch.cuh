@@ -186,6 +186,11 @@ static cudaError_t dispatch(int what, int variant, int tier, int uni, const Step
     }
 #else
     if (tier == TIER_CTA) {
+        if (uni >= 6) {   // speculative single-rod kernels
+            if (variant == 0)
+                return dispatch_spec<Real, 1, 132, TIER_CTA>(what, uni, a, ncta, threads, smem, cluster, st, out);
+            return cudaErrorInvalidValue;
+        }
         switch (variant) {
             case 0: return RSB_D(1, 132, TIER_CTA);
             case 1: return RSB_D(1, 258, TIER_CTA);

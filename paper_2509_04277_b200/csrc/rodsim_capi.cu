@@ -119,6 +119,16 @@ struct Group {       // one kernel launch
     void* d_halo = nullptr;
 };
 
+// groups with speculative kernels: the batched stream variant and the
+// smallest single-rod CTA variant (plain scenes -- the scene-feature kernels
+// keep their fallbacks).  Larger one-CTA rods stay exact: a planar rod's
+// torques carry rounding noise (~1e-300) below the fast path's window, and
+// a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
+bool spec_group(const Group& g) {
+    return (g.tier == TIER_STREAM && g.variant == 7) || (g.tier == TIER_CTA && g.variant == 0);
+}
+
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -782,11 +792,11 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             int per_sm = occ;
             if (const char* e = getenv("RSB_STREAM_CTAS")) per_sm = std::max(1, std::min(occ, atoi(e)));
             g.grid = std::min(g.ncta, per_sm * h->num_sms);
-            if (g.variant == 7 && !h->dry) {   // the speculative launch's redo list
-                int rc2 = dev_alloc(h->redo_list, sizeof(int32_t) * size_t(g.ncta));
-                if (!rc2) rc2 = dev_alloc(h->redo_count, sizeof(int32_t));
-                if (rc2) return rc2;
-            }
+        }
+        if (spec_group(g) && !h->dry) {   // the speculative launch's redo list
+            int rc2 = dev_alloc(h->redo_list, sizeof(int32_t) * size_t(g.ncta));
+            if (!rc2) rc2 = dev_alloc(h->redo_count, sizeof(int32_t));
+            if (rc2) return rc2;
         }
         if (g.tier == TIER_GRID) {
             CK(cudaMalloc(&g.d_flags, sizeof(int32_t) * g.ncta));
@@ -1208,7 +1218,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // quotients never take the IEEE fallback, then the exact kernel over the
     // rods it listed (almost always none: the exact launch finds an empty
     // list and returns)
-    const bool spec = h->spec && g.tier == TIER_STREAM && g.variant == 7 && cfg0 < 3 && h->redo_count.p;
+    const bool spec = h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p;
     if (spec) CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
     auto one = [&](int cfg, int redo_mode) -> cudaError_t {
         auto finish = [&](auto& a) {

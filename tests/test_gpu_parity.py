@@ -470,3 +470,24 @@ def test_speculative_batch_redoes_exactly_the_rods_that_need_it():
         dev.download(_lib.RS_STATE)
     OracleStepper(hr).run(2)
     assert_bitwise(h, hr)
+
+
+def test_speculative_single_rod_redo():
+    # one-CTA rods (variant 0) launch speculatively too: the tiny rod's launch
+    # is handed to the exact kernel, the cantilever's is not after the start
+    from paper_2509_04277_b200 import _lib
+    g, r = _tiny_world(1, 16), _tiny_world(1, 16)
+    with Engine(g) as eng:
+        assert eng.plan()["groups"][0]["variant"] == 0
+        dev = eng.device_world
+        dev.run(5)
+        assert dev.last_redo_count() == 1
+        dev.download(_lib.RS_STATE)
+    OracleStepper(r).run(5)
+    assert_bitwise(g, r)
+    c = wl.cantilever()
+    with Engine(c) as eng:
+        dev = eng.device_world
+        dev.run(100)
+        dev.run(100)
+        assert dev.last_redo_count() == 0
