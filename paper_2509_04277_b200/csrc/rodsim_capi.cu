@@ -124,6 +124,7 @@ struct Group {       // one kernel launch
 // keep their fallbacks).  Larger one-CTA rods stay exact: a planar rod's
 // torques carry rounding noise (~1e-300) below the fast path's window, and
 // a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
+constexpr int kSpecMinSteps = 32;
 bool spec_group(const Group& g) {
     return (g.tier == TIER_STREAM && g.variant == 7) || (g.tier == TIER_CTA && g.variant == 0);
 }
@@ -1218,7 +1219,10 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // quotients never take the IEEE fallback, then the exact kernel over the
     // rods it listed (almost always none: the exact launch finds an empty
     // list and returns)
-    const bool spec = h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p;
+    // (one-CTA rods only for long epochs: the exact launch over the redo
+    // list costs a few microseconds, a whole K = 1 step on a short rod)
+    const bool spec = h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
+                      (g.tier != TIER_CTA || steps >= kSpecMinSteps);
     if (spec) CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
     auto one = [&](int cfg, int redo_mode) -> cudaError_t {
         auto finish = [&](auto& a) {

@@ -480,10 +480,10 @@ def test_speculative_single_rod_redo():
     with Engine(g) as eng:
         assert eng.plan()["groups"][0]["variant"] == 0
         dev = eng.device_world
-        dev.run(5)
+        dev.run(40)   # one-CTA rods speculate in epochs of >= 32 steps
         assert dev.last_redo_count() == 1
         dev.download(_lib.RS_STATE)
-    OracleStepper(r).run(5)
+    OracleStepper(r).run(40)
     assert_bitwise(g, r)
     c = wl.cantilever()
     with Engine(c) as eng:
