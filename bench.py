@@ -543,19 +543,30 @@ def run_ours(args):
     ms10 = D.max(dev.timer_ms())
     value_k10 = args.rods * ELEMENTS * 30 / (ms10 * 1e-3)
 
-    # ---- NCCL gather of the final positions (results only) -----------
-    gathered = None
-    if world > 1:
-        import torch
-        ptr = dev.device_ptr(0)
-        src = torch.as_tensor(_CudaArray(ptr, (P * 3,), "<f8" if real == 8 else "<f4"),
+    # ---- NCCL gather of the final state (results only) ---------------
+    # positions (P,3) and frames (E,4) of every rank's shard, concatenated in
+    # rod order on rank 0; the digest of the gathered bits
+    # lets the tests compare an N-rank run with a single-process one
+    import hashlib
+    import torch
+    gathered = 0
+    digest = hashlib.sha256()
+    tdt = torch.float64 if real == 8 else torch.float32
+    for which, n in ((0, P * 3), (2, E * 4)):
+        src = torch.as_tensor(_CudaArray(dev.device_ptr(which), (n,), "<f8" if real == 8 else "<f4"),
                               device=f"cuda:{local}")
-        if D.backend != "nccl":   # gloo test path: gather through host memory
-            src = src.cpu()
-        out = torch.empty(world * P * 3, dtype=src.dtype, device=src.device)
-        D.dist.all_gather_into_tensor(out, src.contiguous())
+        assert src.dtype == tdt
+        if world > 1:
+            if D.backend != "nccl":   # gloo test path: gather through host memory
+                src = src.cpu()
+            out = torch.empty(world * n, dtype=src.dtype, device=src.device)
+            D.dist.all_gather_into_tensor(out, src.contiguous())
+        else:
+            out = src
         torch.cuda.synchronize()
-        gathered = int(out.numel())
+        gathered += int(out.numel())
+        if rank == 0:
+            digest.update(out.cpu().numpy().tobytes())
 
     if rank == 0:
         line = {
@@ -592,8 +603,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "build_s": t_build,
         }
-        if gathered is not None:
-            line["nccl_gather_elems"] = gathered
+        line["nccl_gather_elems"] = gathered
+        line["state_sha256"] = digest.hexdigest()
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
         if world == 1 and not args.no_single:

@@ -19,6 +19,7 @@
  * rs_error_step                    _core.error_step            _core.pyx:1142
  * rs_step_counter                  _core.step_counter          _core.pyx:1147
  * rs_update_params                 _core.update_params         _core.pyx:1083
+ * rs_barrier_timing                barrier wait accounting     _core.pyx:453-471
  * rs_stage_commands                _core.stage_commands        _core.pyx:1151
  * rs_applied_step_for              _core.applied_step_for      _core.pyx:1181
  * rs_read_snapshot                 SnapshotBuffer.read         engine.py:113
@@ -136,7 +137,10 @@ int rs_upload(rs_handle h, uint32_t mask);
  * Applies commands staged with rs_stage_commands at the first step boundary.
  * contacts: active mesh contacts + self-collision pairs after the last
  * step (epoch_results, _core.pyx:1133; waits for the epoch when the scene
- * has contacts); barrier_ns: 0 (barriers are on-chip).
+ * has contacts); barrier_ns: with rs_barrier_timing on, the summed time the
+ * CTAs (thread 0 of each) spent waiting in the step's barriers, the
+ * counterpart of the reference's per-block spin-barrier wait
+ * (_core.pyx:453-471, epoch_results 1133-1139; waits for the epoch); else 0.
  * Either pointer may be NULL. */
 int rs_run_epoch(rs_handle h, int64_t steps, int64_t *contacts, int64_t *barrier_ns);
 int rs_download(rs_handle h, uint32_t mask);
@@ -152,6 +156,11 @@ int rs_synchronize(rs_handle h);
 int64_t rs_error_step(rs_handle h);
 int64_t rs_step_counter(rs_handle h);
 int rs_update_params(rs_handle h, double dt, int64_t iters);
+/* 1: account barrier waits (rs_run_epoch's barrier_ns) -- launches use the
+ * scene-feature kernels, whose barriers read the SM clock around the wait;
+ * batched stream-tier launches (independent rods, one CTA each) report 0.
+ * 0 (default): no accounting, the plain kernels. */
+int rs_barrier_timing(rs_handle h, int on);
 /* ops: (n,6) rows [op, i0, i1, f0, f1, f2], ops 0..3 = driver velocity,
  * driver rotation, grab, release (engine.py:30-34). slots: (n) out. */
 int rs_stage_commands(rs_handle h, const double *ops, int64_t n, int64_t *slots);

@@ -173,6 +173,17 @@ class OracleStepper:
         self.lib.ro_run(ctypes.byref(self.s), int(steps))
         self.world.step_index += int(steps)
 
+    def set_params(self, dt=None, iterations=None):
+        """Engine.set_params between epochs (engine.py:335-355): the World's
+        dt / solver.iterations and the context's copies
+        (_core.update_params, _core.pyx:1083-1089)."""
+        if dt is not None:
+            self.world.dt = float(dt)
+        if iterations is not None:
+            self.world.solver.iterations = int(iterations)
+        self.s.dt = self.world.dt
+        self.s.iters = self.world.solver.iterations
+
     @property
     def error_step(self):
         return int(self.s.err_step)
@@ -230,6 +241,13 @@ class ReferenceStepper:
         for _ in range(int(steps)):
             self.core.step_serial(self.ctx)
             self.world.step_index += 1
+
+    def set_params(self, dt=None, iterations=None):
+        if dt is not None:
+            self.world.dt = float(dt)
+        if iterations is not None:
+            self.world.solver.iterations = int(iterations)
+        self.core.update_params(self.ctx, self.world.dt, self.world.solver.iterations)
 
     @property
     def error_step(self):

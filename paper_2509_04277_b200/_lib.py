@@ -104,6 +104,7 @@ SIGNATURES = [
     ("rs_plan_dry", _i32, [ctypes.POINTER(WorldDesc), _i32, ctypes.c_char_p, _i64]),
     ("rs_micro", _i32, [_i32, _i32, ctypes.POINTER(_f64)]),
     ("rs_live_snapshots", _i32, [_p, _i32]),
+    ("rs_barrier_timing", _i32, [_p, _i32]),
 ]
 
 MICRO_KINDS = {"dadd": 0, "dmul": 1, "dfma": 2, "div": 3, "sqrt_add": 4, "div_rn": 5,
@@ -325,6 +326,10 @@ class DeviceWorld:
 
     def update_params(self, dt, iters):
         check(self.lib.rs_update_params(self.handle, float(dt), int(iters)), self.lib)
+
+    def barrier_timing(self, on=True):
+        """Account barrier waits in run()'s barrier_ns (rs_barrier_timing)."""
+        check(self.lib.rs_barrier_timing(self.handle, int(bool(on))), self.lib)
 
     def stage_commands(self, ops):
         ops = np.ascontiguousarray(ops, dtype=np.float64)

@@ -171,6 +171,10 @@ struct StepArgs {
     LiveSnap* snap;                                // live per-step snapshot (or null)
     double *snap_pos, *snap_q;                     // (2, P, 3), (2, E, 4)
     int64_t snap_base, snap_P, snap_E;             // version at launch start, sizes
+    // barrier wait accounting (the reference's per-block barrier_wait_ns,
+    // _core.pyx:453-471): scene-feature kernels only; thread 0 of every CTA
+    // adds the SM cycles it spent inside barriers (null: off)
+    unsigned long long* bar_cycles;
 };
 
 constexpr int PROF_SLOTS = 64;

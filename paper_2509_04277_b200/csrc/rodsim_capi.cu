@@ -173,6 +173,10 @@ struct rs_handle_s {
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;   // pinned
     unsigned long long* d_prof = nullptr;  // RSB_DEBUG bit 1: per-phase cycles (CTA 0)
+    bool bar_timing = false;               // rs_barrier_timing: barrier wait cycles
+    unsigned long long* d_bar = nullptr;
+    unsigned long long* h_bar = nullptr;   // pinned
+    int clock_khz = 0;                     // SM clock for cycles -> ns
     int64_t prof_steps = 0;
     int has_fext = 0;
 
@@ -352,8 +356,15 @@ int64_t rod_of(const rs_world_desc& d, int64_t p) {
 // ---- launch planning --------------------------------------------------------
 
 // kernel configuration: material-constant storage + scene features
+// (barrier timing: the feature kernels, where the group's variant has one)
+bool has_feat_kernel(const Group& g) {
+    return g.tier == TIER_CLUSTER || g.tier == TIER_GRID ||
+           (g.tier == TIER_CTA && g.variant <= 4 && g.variant != 3);
+}
+
 int launch_cfg(rs_handle h, const Group& g) {
-    const bool feat = (h->contacts_on || h->d.has_self || h->live) && g.tier != TIER_STREAM;
+    const bool feat = ((h->contacts_on || h->d.has_self || h->live) && g.tier != TIER_STREAM) ||
+                      (h->bar_timing && has_feat_kernel(g));
     return g.uni + (feat ? 3 : 0);
 }
 
@@ -1204,6 +1215,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.gx = Real(h->d.gx);
     a.gy = Real(h->d.gy);
     a.gz = Real(h->d.gz);
+    a.bar_cycles = h->bar_timing ? h->d_bar : nullptr;
     return a;
 }
 
@@ -1300,7 +1312,14 @@ int epoch_epilogue(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barri
             *contacts = int64_t(*h->h_contacts);
         }
     }
-    if (barrier_ns) *barrier_ns = 0;
+    if (barrier_ns) {
+        *barrier_ns = 0;
+        if (h->bar_timing) {   // epoch_results' barrier sum: cycles at the SM clock
+            CK(cudaMemcpyAsync(h->h_bar, h->d_bar, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaStreamSynchronize(h->st));
+            *barrier_ns = int64_t(double(*h->h_bar) * 1e6 / double(std::max(h->clock_khz, 1)));
+        }
+    }
     return RS_OK;
 }
 
@@ -1349,6 +1368,7 @@ int run_epoch_pipelined(rs_handle h, int64_t steps, int64_t* contacts, int64_t* 
     CK(cudaEventRecord(h->ev_k[C], h->st));
     CK(cudaStreamWaitEvent(h->st_in, h->ev_k[C], 0));
     if (h->timing) CK(cudaEventRecord(h->ev0, h->st));
+    if (h->bar_timing) CK(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned long long), h->st));
     double* const hp[4] = {d.pos, d.vel, d.q, d.w};
     DevBuf* const dp[4] = {&h->pos, &h->vel, &h->q, &h->w};
     const int width[4] = {3, 3, 4, 3};
@@ -1501,6 +1521,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
     int rc = epoch_prelude(h);
     if (rc) return rc;
     if (h->timing) CK(cudaEventRecord(h->ev0, h->st));
+    if (h->bar_timing) CK(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned long long), h->st));
     int64_t done = 0;
     while (done < steps) {
         const int k = int(std::min<int64_t>(steps - done, kMaxStepsPerLaunch));
@@ -1641,6 +1662,18 @@ int rs_update_params(rs_handle h, double dt, int64_t iters) {
     return RS_OK;
 }
 
+int rs_barrier_timing(rs_handle h, int on) {
+    if (!h) return fail(RS_E_INVALID, "null handle");
+    CK(cudaSetDevice(h->d.device));
+    if (on && !h->d_bar) {
+        CK(cudaMalloc(&h->d_bar, sizeof(unsigned long long)));
+        CK(cudaMallocHost(&h->h_bar, sizeof(unsigned long long)));
+        CK(cudaDeviceGetAttribute(&h->clock_khz, cudaDevAttrClockRate, h->d.device));
+    }
+    h->bar_timing = on != 0;
+    return RS_OK;
+}
+
 int rs_stage_commands(rs_handle h, const double* ops, int64_t n, int64_t* slots) {
     if (!h || (n > 0 && !ops)) return fail(RS_E_INVALID, "null argument");
     std::lock_guard<std::mutex> lk(h->ring_mu);
@@ -1745,6 +1778,8 @@ void rs_destroy(rs_handle h) {
     if (h->d_contacts) cudaFree(h->d_contacts);
     if (h->d_pairs) cudaFree(h->d_pairs);
     if (h->h_contacts) cudaFreeHost(h->h_contacts);
+    if (h->d_bar) cudaFree(h->d_bar);
+    if (h->h_bar) cudaFreeHost(h->h_bar);
     if (h->stage) cudaFreeHost(h->stage);
     if (h->ring) cudaFreeHost(h->ring);
     if (h->snap) cudaFreeHost(h->snap);

@@ -202,6 +202,10 @@ class Engine:
                                      force_tier=ft, force_ctas=fc,
                                      force_variant=fv, live=self._want_live)
         self._live = bool(self._dev.plan().get("live", False))
+        # the parallel backend reports barrier waits (engine.py:300-313: the
+        # serial backend's barrier_wait_ns is 0, it has no barriers)
+        if self.backend == "parallel":
+            self._dev.barrier_timing(True)
         self._live_snaps = False
         self._bound = {a: getattr(self.world, a) for a in _BOUND_ATTRS}
         # the mesh and the collision scalars are bound too (make_context)

@@ -95,15 +95,22 @@ def recipes(rs):
             w.clamp_point(r, 0)
         return w
 
-    # name -> (builder, checkpoints, epoch size)
+    # name -> (builder, checkpoints, epoch size[, {step: set_params kwargs}])
+    # The set_params scripts change dt / iterations between epochs through
+    # the reference Engine (engine.py:335-355 -> _core.update_params,
+    # _core.pyx:1083-1089) at the given step boundaries.
     return {
         "cfg1_cantilever64": (lambda: cantilever(), (1, 10, 100, 1000), 1000),
         "cfg2_extensible512": (lambda: cantilever(512, 1.0, stretch_modulus=1e6,
-                                                  extensible=True), (10, 100, 300), 10),
-        "cfg3_pair2x512": (pair, (10, 100, 300), 10),
+                                                  extensible=True), (10, 100, 300, 1000), 10),
+        "cfg3_pair2x512": (pair, (10, 100, 300, 1000), 10),
         "cfg4_sweep256": (lambda: cantilever(256, 0.512), (100,), 100),
         "cfg4_sweep2048": (lambda: cantilever(2048, 4.096), (20,), 10),
         "cfg5_hair8": (hair, (100, 1000), 100),
+        "cfg1_set_params": (lambda: cantilever(), (100, 200, 300), 50,
+                            {100: dict(dt=5e-5, iterations=6), 200: dict(dt=1.5e-4, iterations=14)}),
+        "cfg3_set_params": (pair, (100, 200, 300), 10,
+                            {100: dict(iterations=4), 200: dict(dt=5e-5, iterations=12)}),
     }
 
 
@@ -114,16 +121,22 @@ def digest(arrays):
     return h.hexdigest()
 
 
-def main():
+def main(only=None):
     rs = import_reference()
     from rodsim.engine import Engine
-    for name, (build, checkpoints, epoch) in recipes(rs).items():
+    for name, recipe in recipes(rs).items():
+        if only and name not in only:
+            continue
+        build, checkpoints, epoch = recipe[:3]
+        script = recipe[3] if len(recipe) > 3 else {}
         w = build()
         out = {f"init_{k}": np.array(getattr(w, k)) for k in STATE + STATIC}
         done = 0
         with Engine(w, backend="serial") as eng:
             for c in checkpoints:
                 while done < c:
+                    if done in script:
+                        eng.set_params(**script[done])
                     k = min(epoch, c - done)
                     eng.run_epoch(k)
                     done += k
@@ -131,6 +144,8 @@ def main():
                     out[f"step{c}_{k}"] = np.array(getattr(w, k))
                 out[f"step{c}_sha256"] = np.array(digest(getattr(w, k) for k in STATE))
         out["checkpoints"] = np.array(checkpoints)
+        for s_, kw in script.items():
+            out[f"set_params_{s_}"] = np.array([kw.get("dt", np.nan), kw.get("iterations", -1)], dtype=np.float64)
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **out)
         print(f"{name}: P={w.num_points} checkpoints={checkpoints} "
@@ -172,6 +187,8 @@ if __name__ == "__main__":
         copy_knot_assets()
     elif "--assets" in sys.argv:
         copy_scenario_assets()
+    elif len(sys.argv) > 1:
+        main(set(sys.argv[1:]))   # regenerate the named fixtures only
     else:
         main()
         copy_knot_assets()

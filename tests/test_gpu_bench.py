@@ -45,4 +45,12 @@ def test_bench_two_ranks_one_device():
                          timeout=600).stdout
     d = _line(out)
     assert d["n_gpus"] == 2 and d["config"]["rods_per_gpu"] == 2048
-    assert d["nccl_gather_elems"] == 4096 * 129 * 3 and "cpu_baseline" not in d
+    assert d["nccl_gather_elems"] == 4096 * (129 * 3 + 128 * 4) and "cpu_baseline" not in d
+    # the gathered positions + frames equal one process stepping the whole
+    # batch through the same sequence of epochs, bit for bit
+    one = subprocess.run([sys.executable, "bench.py", "--rods", "4096", "--steps", "3", "--warmup", "3",
+                          "--no-single", "--no-cpu", "--e2e-steps", "1"], cwd=ROOT, check=True,
+                         capture_output=True, text=True, timeout=600).stdout
+    s = _line(one)
+    assert s["nccl_gather_elems"] == d["nccl_gather_elems"]
+    assert s["state_sha256"] == d["state_sha256"]

@@ -303,3 +303,60 @@ def test_partition_kats_and_properties():
     assert partition_world(w, cap=10, max_blocks=3).block_count == 6   # 3 per rod
     starts, ends = block_ranges(part)
     assert starts.dtype == np.int64 and list(starts) == [0, 34, 67, 100, 125]
+
+
+# -- numpy twin of the step: forces.* + integrate_* (forces.py:134-236) -------
+
+def test_numpy_twin_integrators_track_the_oracle():
+    # An all-extensible free rod has no distance projection, so one step is
+    # elastic forces + damping + gravity -> integrate_velocities ->
+    # integrate_positions; the numpy twin agrees with the compiled step to
+    # rounding (the reference's own check: test_engine.py:175-182, 1e-12).
+    from oracle.oracle import OracleStepper
+    from paper_2509_04277_b200 import workloads as wl
+    p = st.RodParams(**dict(wl.MATERIAL, extensible=True, stretch_modulus=1e6))
+
+    def make():
+        w = World(dt=1e-4, gravity=(0.0, -9.81, 0.0), solver=SolverConfig(iterations=3))
+        w.add_rod(st.init_rod(20, 0.2, axis=(1.0, 0.3, 0.1)), p)
+        w.finalize()
+        r = np.random.default_rng(1)
+        w.velocities[:] = r.normal(size=w.velocities.shape) * 1e-2
+        w.angular_velocities[:] = r.normal(size=w.angular_velocities.shape) * 1e-1
+        return w
+
+    a, b = make(), make()
+    OracleStepper(a).run(50)
+    s = b.rod_state(0)
+    for _ in range(50):
+        buf = forces.elastic_forces_torques(s, p)
+        forces.add_damping(s, p, buf)
+        buf.forces += b.masses[:, None] * np.asarray(b.gravity)
+        forces.integrate_velocities(s, buf, b.masses, b.inertias, b.dt)
+        forces.integrate_positions(s, b.dt)
+    assert np.max(np.abs(s.positions - a.positions)) <= 1e-12
+    assert np.max(np.abs(s.frames - a.frames)) <= 1e-12
+    assert np.max(np.abs(s.velocities - a.velocities)) <= 1e-12
+    assert np.max(np.abs(s.angular_velocities - a.angular_velocities)) <= \
+        1e-9 * np.max(np.abs(a.angular_velocities))
+
+
+def test_integrators_locks_and_arguments():
+    s = st.init_rod(5, 0.4)
+    buf = forces.ForceTorqueBuffer.zeros(5)
+    buf.forces[:] = 1.0
+    buf.body_torques[:] = 2.0
+    m, inert = np.full(5, 0.5), np.full((4, 3), 0.25)
+    plock, flock = np.zeros(5, bool), np.zeros(4, bool)
+    plock[0] = flock[1] = True
+    forces.integrate_velocities(s, buf, m, inert, 0.1, plock, flock)
+    assert np.all(s.velocities[0] == 0.0) and np.allclose(s.velocities[1:], 0.2)
+    assert np.all(s.angular_velocities[1] == 0.0) and np.allclose(s.angular_velocities[0], 0.8)
+    p0 = s.positions.copy()
+    forces.integrate_positions(s, 0.1)
+    assert np.allclose(s.positions, p0 + 0.1 * s.velocities)
+    assert np.allclose(np.linalg.norm(s.frames, axis=1), 1.0)
+    with pytest.raises(ValueError):
+        forces.integrate_positions(s, 0.0)
+    with pytest.raises(ValueError):
+        forces.integrate_velocities(s, buf, m, inert, -1.0)

@@ -25,20 +25,12 @@ from paper_2509_04277_b200 import workloads as wl
 from paper_2509_04277_b200.constraints import SolverConfig
 from paper_2509_04277_b200.world import BIND_BIDIRECTIONAL, BIND_ONE_WAY, World
 
-GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-STATE = ("positions", "velocities", "frames", "angular_velocities")
-BUILDERS = {
-    "cfg1_cantilever64": wl.cantilever,
-    "cfg2_extensible512": wl.extensible,
-    "cfg3_pair2x512": wl.pair,
-    "cfg4_sweep256": lambda: wl.sweep(256),
-    "cfg4_sweep2048": lambda: wl.sweep(2048),
-    "cfg5_hair8": lambda: wl.hair(8),
-}
+import golden_fixtures as gf
 
-
-def golden(name):
-    return np.load(os.path.join(GOLDEN, f"{name}.npz"))
+GOLDEN = gf.GOLDEN
+STATE = gf.STATE
+BUILDERS = {name: make for name, (make, _) in gf.BUILDERS.items()}
+golden = gf.load
 
 
 def test_every_fixture_has_a_builder():
@@ -70,17 +62,20 @@ def test_oracle_reproduces_reference_checkpoints(name):
     g = golden(name)
     w = BUILDERS[name]()
     stepper = OracleStepper(w)
-    done = 0
-    for c in g["checkpoints"]:
-        stepper.run(int(c) - done)
-        done = int(c)
+
+    def check(c):
         for k in STATE:
             assert np.array_equal(getattr(w, k), g[f"step{c}_{k}"]), (c, k)
         h = hashlib.sha256()
         for k in STATE:
             h.update(np.ascontiguousarray(getattr(w, k)).tobytes())
         assert h.hexdigest() == str(g[f"step{c}_sha256"])
+
+    # the oracle steps one epoch of any length bitwise like K single steps
+    gf.replay(g, 10 ** 9, stepper.run, stepper.set_params, check)
     assert stepper.error_step == -1
+    if gf.script(g):   # the parameter changes really changed the trajectory
+        assert w.dt == g["set_params_200"][0]
 
 
 # -- oracle vs the reference's compiled core on randomized scenes -------------
