@@ -13,16 +13,16 @@ Headline line (one JSON line on rank 0):
           (cfg1, cfg2, cfg3 pair incl. the 1 kHz haptic frame loop, cfg4
           sweep) with the reference CPU core timed beside it.
   roofline    dominant kernel, HBM bytes against MEASURED_PEAKS.json.
-  cpu_baseline  the reference's own compiled core (oracle/_ref) or the C
-          restatement, on the box's host cores, bounded sample.
+  cpu_baseline  the unmodified reference package (baseline/_ref, its own
+          Engine API; bench_reference.py) on all host cores, on the same
+          full batch (5 timed steps).
 
 `--impl reference` times the reference CPU implementation on the same
-metric/config (rank 0 only; other ranks exit).
+metric/config (rank 0 only; other ranks exit): bench_reference.batch_arm.
 """
 
 import argparse
 import json
-import multiprocessing as mp
 import os
 import statistics
 import subprocess
@@ -219,54 +219,6 @@ class ClockSampler:
                 "samples": len(self.sm), "source": self.source}
 
 
-# ---- CPU baseline: the reference core on host cores -------------------------
-
-def _cpu_worker(args):
-    rods, first, steps, kind = args
-    sys.path.insert(0, ROOT)
-    from oracle.oracle import OracleStepper, ReferenceStepper
-    from paper_2509_04277_b200 import workloads
-    w = workloads.hair(rods, ELEMENTS, first=first)
-    stepper = ReferenceStepper(w) if kind == "reference" else OracleStepper(w)
-    stepper.run(1)   # warm-up
-    t0 = time.perf_counter()
-    stepper.run(steps)
-    dt = time.perf_counter() - t0
-    return rods * ELEMENTS * steps, dt
-
-
-def cpu_kind():
-    from oracle.oracle import reference_core_path
-    return "reference" if reference_core_path() else "port"
-
-
-def cpu_baseline(procs, rods_per_proc=192, steps=20, repeats=1):
-    """Element-steps/s of the reference CPU path on `procs` processes (one
-    World shard per process, Engine(backend="serial") semantics)."""
-    kind = cpu_kind()
-    ctx = mp.get_context("fork")
-    best = 0.0
-    with ctx.Pool(procs) as pool:
-        for _ in range(repeats):
-            out = pool.map(_cpu_worker, [(rods_per_proc, i * rods_per_proc, steps, kind)
-                                         for i in range(procs)])
-            best = max(best, sum(n / t for n, t in out))
-    return {"value": best, "unit": "element-steps/s", "cores": procs, "kind": kind,
-            "sample": f"hair {rods_per_proc} rods x {ELEMENTS} el x {steps} steps "
-                      f"per process, {procs} processes (best of {repeats})"}
-
-
-def cpu_single_rod_us(make, steps):
-    from oracle.oracle import OracleStepper, ReferenceStepper
-    kind = cpu_kind()
-    w = make()
-    s = ReferenceStepper(w) if kind == "reference" else OracleStepper(w)
-    s.run(2)
-    t0 = time.perf_counter()
-    s.run(steps)
-    return (time.perf_counter() - t0) / steps * 1e6, kind
-
-
 # ---- distributed plumbing ---------------------------------------------------
 
 def dist_env():
@@ -323,6 +275,47 @@ class _CudaArray:
 
 # ---- single-rod latency measurements (rank 0, N = 1) ------------------------
 
+# Dependent-chain length of each phase of one step (SURVEY §8(d) t_chain),
+# counted from the kernel's critical path (rod_step.cuh; the longest chain
+# from the phase's first shared-memory load to its last store):
+#   d     dependent fp64 add/mul/fma    sqrt, rcp   the square root / 1/x
+#   lds   shared-memory loads on the chain (DSMEM when the slot is remote)
+# scatter:   pos load -> d -> |d|^2 (mul, 2 add) -> sqrt -> 1/|d| -> t
+#            (div_fast: 3) -> er -> er.t (3) -> pair (4) -> ef (1)       16 d
+#            (+6 for the stretch term of an extensible element)
+# gather:    F = ff_own + ff_next(e-1) -> F.q (4) -> F - (F.q)q (2) ->
+#            vec(conj(q)F) (4) -> x0.5 -> +jtau -jtau(e-1) -> tau - gyro ->
+#            dt x -> div_fast (3) -> w + dw                            20 d
+# integrate: q (x) (0,w) (4) -> q + h dq (2) -> |q|^2 (4) -> sqrt -> 1/x
+#            -> div_fast (3)                                            15 d
+# colour:    v loads -> vb - va -> x n -> +, + -> + bias -> lambda
+#            (mul, fma, fma) -> im lambda -> x n -> va -                11 d
+# binding:   v loads -> vrel (4) -> + bias -> lambda (3) -> w lam n (2) -> +  11 d
+# contact:   normal impulse with accumulator + box friction            ~24 d + 1 div
+PHASE_CHAIN = {
+    "scatter": {"d": 16, "sqrt": 1, "rcp": 1, "lds": 1},
+    "gather": {"d": 20, "lds": 1},
+    "integrate": {"d": 15, "sqrt": 1, "rcp": 1, "lds": 1},
+    "colour": {"d": 11, "lds": 1},
+    "binding": {"d": 11, "lds": 1},
+    "contact": {"d": 24, "div": 1, "lds": 1},
+}
+
+
+def micro_latencies():
+    """Measured dependent latencies (cycles) and the SM clock (rs_micro)."""
+    from paper_2509_04277_b200 import _lib
+    lat = {}
+    for key, kind in (("d", "dadd"), ("sqrt", "sqrt_add"), ("rcp", "rcp"), ("div", "div"),
+                      ("lds", "lds"), ("dsmem", "dsmem")):
+        cyc, ns = _lib.micro(kind)
+        lat[key] = cyc
+        if key == "d" and ns > 0:
+            lat["ghz"] = cyc / ns
+    lat["sqrt"] = max(lat["sqrt"] - lat["d"], 0.0)   # the kind-4 chain is sqrt + add
+    return lat
+
+
 def barrier_ns(plan):
     """Measured cost of one phase barrier of a plan's tier (rs_micro)."""
     from paper_2509_04277_b200 import _lib
@@ -331,17 +324,42 @@ def barrier_ns(plan):
     return _lib.micro("bar_sync", plan["threads"])[1]
 
 
-def latency_floor(plan, us, iters=10, binds=False):
-    """Synchronisation floor of one step: n_sync phase barriers (2I+3, 3I+3
-    with bindings) at the measured barrier latency of
-    the tier -- t_floor without the per-phase dependency chains."""
-    n_sync = (3 if binds else 2) * iters + 3
-    floor = n_sync * barrier_ns(plan) / 1e3
-    return {"n_sync": n_sync, "barrier_ns": barrier_ns(plan), "sync_floor_us": floor,
-            "frac": floor / us}
+def latency_floor(plan, us, k, lat, iters=10, ext=False, t_launch_us=0.0):
+    """t_floor = n_sync t_sync + t_chain + t_launch / K.
+    n_sync: the barriers the kernel issues per step (from the plan: 3 + I x
+    (2 colour phases when any element is distance-projected, + contacts,
+    self-collision pairs, bindings, grabs)); t_sync: the tier's measured
+    barrier; t_chain: the phases' dependent chains at the measured latencies
+    (PHASE_CHAIN; halo loads of a multi-CTA tier are DSMEM reads)."""
+    n_sync = plan["sync_per_step"]
+    t_sync = barrier_ns(plan)
+
+    def cyc(ph, extra_d=0):
+        # (a multi-CTA tier's halo loads are DSMEM reads; its measured t_sync
+        # already includes one DSMEM read per phase, so they count as LDS here)
+        c = PHASE_CHAIN[ph]
+        ld = lat["lds"]
+        return ((c.get("d", 0) + extra_d) * lat["d"] + c.get("sqrt", 0) * lat["sqrt"] +
+                c.get("rcp", 0) * lat["rcp"] + c.get("div", 0) * lat["div"] + c.get("lds", 0) * ld)
+    chain = cyc("scatter", 6 if ext else 0) + cyc("gather") + cyc("integrate")
+    per_it = 0.0
+    if plan["sync_per_iteration"] >= 2 and (plan["any_dist"] or plan["bindings"]):
+        per_it += 2 * cyc("colour")
+    if plan["bindings"]:
+        per_it += cyc("binding")
+    if plan["contacts"]:
+        per_it += cyc("contact")
+    chain += iters * per_it
+    t_chain_us = chain / lat["ghz"] / 1e3
+    t_sync_us = n_sync * t_sync / 1e3
+    floor = t_sync_us + t_chain_us + t_launch_us / k
+    return {"n_sync": n_sync, "t_sync_ns": t_sync, "sync_us": t_sync_us, "t_chain_us": t_chain_us,
+            "chain_cycles": chain, "t_launch_us": t_launch_us, "k": k, "t_floor_us": floor,
+            "frac": floor / us, "model": "n_sync t_sync + t_chain + t_launch/K"}
 
 
 def single_rod_suite(precision):
+    import bench_reference as br
     from paper_2509_04277_b200 import workloads as wl
     from paper_2509_04277_b200.engine import Engine
 
@@ -359,19 +377,27 @@ def single_rod_suite(precision):
             plan = eng.plan()["groups"][0]
         return ms * 1e3 / (k * launches), plan
 
-    out = {}
-    us, plan = device_us(wl.cantilever, 1000, 3)
-    cpu, kind = cpu_single_rod_us(wl.cantilever, 1000)
-    out["cfg1_cantilever_64"] = {"us_per_step": us, "k": 1000, "tier": plan["tier"],
-                                 "cpu_us_per_step": cpu, "cpu_kind": kind,
-                                 "roofline": latency_floor(plan, us)}
-    us, plan = device_us(wl.extensible, 10, 100)
-    cpu, _ = cpu_single_rod_us(wl.extensible, 200)
-    out["cfg2_extensible_512"] = {"us_per_step": us, "k": 10, "tier": plan["tier"],
-                                  "cpu_us_per_step": cpu, "roofline": latency_floor(plan, us)}
-    us, plan = device_us(wl.pair, 10, 100)
-    pair_plan = plan
-    cpu, _ = cpu_single_rod_us(wl.pair, 100)
+    lat = micro_latencies()
+    # launch overhead: one launch per step minus the per-step cost at K = 100
+    us1, _ = device_us(lambda: wl.sweep(16), 1, 200)
+    us100, _ = device_us(lambda: wl.sweep(16), 100, 20)
+    t_launch = max(us1 - us100, 0.0)
+    out = {"latencies_cycles": lat, "t_launch_us": t_launch}
+
+    def row(name, make, k, launches, cpu_name, cpu_args=(), cpu_steps=200, ext=False, **extra):
+        us, plan = device_us(make, k, launches)
+        r = {"us_per_step": us, "k": k, "tier": plan["tier"], "ctas": plan["ctas"],
+             "roofline": latency_floor(plan, us, k, lat, ext=ext, t_launch_us=t_launch)}
+        r.update(br.single_rod_cpu(cpu_name, cpu_args, steps=cpu_steps))
+        r["speedup_vs_cpu"] = r["cpu_us_per_step"] / us
+        r.update(extra)
+        out[name] = r
+        return r
+
+    row("cfg1_cantilever_64", wl.cantilever, 1000, 3, "cantilever", cpu_steps=1000)
+    row("cfg2_extensible_512", wl.extensible, 10, 100, "extensible", ext=True)
+    pair = row("cfg3_pair_2x512", wl.pair, 10, 100, "pair", cpu_steps=100)
+    pair["steps_per_s"] = 1e6 / pair["us_per_step"]
     # haptic frame loop: commands in, K = 10 steps (1 ms simulated), state out
     w = wl.pair()
     frames = []
@@ -385,33 +411,28 @@ def single_rod_suite(precision):
             frames.append(time.perf_counter() - t0)
             _ = float(tip[2])
     frames = np.array(frames[100:]) * 1e6
-    out["cfg3_pair_2x512"] = {
-        "us_per_step": us, "k": 10, "tier": pair_plan["tier"], "ctas": pair_plan["ctas"],
-        "steps_per_s": 1e6 / us, "cpu_us_per_step": cpu,
-        "roofline": latency_floor(pair_plan, us, binds=True),
-        "haptic_frame_us": {"median": float(np.median(frames)),
-                            "p99": float(np.percentile(frames, 99)),
-                            "frames": int(frames.size),
-                            "rate_hz_median": float(1e6 / np.median(frames))}}
+    pair["haptic_frame_us"] = {"median": float(np.median(frames)),
+                               "p99": float(np.percentile(frames, 99)),
+                               "frames": int(frames.size),
+                               "rate_hz_median": float(1e6 / np.median(frames))}
     # the paper's insertion scene: mesh contacts
-    us, plan = device_us(wl.insertion, 100, 10)
-    cpu, _ = cpu_single_rod_us(wl.insertion, 200)
-    out["insertion_128_tube"] = {"us_per_step": us, "k": 100, "tier": plan["tier"],
-                                 "cpu_us_per_step": cpu, "roofline": latency_floor(plan, us),
-                                 "mesh_triangles": 15360, "collision_interval": 4}
+    row("insertion_128_tube", wl.insertion, 100, 10, "insertion", mesh_triangles=15360,
+        collision_interval=4)
     sweep = {}
     for n in (16, 64, 256, 1024, 4096, 16384):
-        row = {}
+        r = {}
         for k in (1, 10, 100):
             launches = max(2, min(200, 2000 // k))
             us, plan = device_us(lambda: wl.sweep(n), k, launches)
-            row[f"k{k}"] = us
-        row["tier"] = plan["tier"]
-        row["ctas"] = plan["ctas"]
-        row["roofline_k100"] = latency_floor(plan, row["k100"])
-        row["cpu_us_per_step"], _ = cpu_single_rod_us(lambda: wl.sweep(n),
-                                                      max(3, 20000 // n))
-        sweep[str(n)] = row
+            r[f"k{k}"] = us
+        r["tier"] = plan["tier"]
+        r["ctas"] = plan["ctas"]
+        r["roofline_k100"] = latency_floor(plan, r["k100"], 100, lat, t_launch_us=t_launch)
+        r["roofline_k1"] = latency_floor(plan, r["k1"], 1, lat, t_launch_us=t_launch)
+        c = br.single_rod_cpu("sweep", (n,), steps=max(3, 20000 // n), par_steps=max(3, 5000 // n))
+        r.update(c)
+        r["speedup_vs_cpu_k100"] = c["cpu_us_per_step"] / r["k100"]
+        sweep[str(n)] = r
     out["cfg4_sweep_us_per_step"] = sweep
     return out
 
@@ -419,40 +440,27 @@ def single_rod_suite(precision):
 # ---- arms ---------------------------------------------------------------------
 
 def run_reference(args):
+    """The reference arm: the unmodified reference package (baseline/_ref)
+    through its own API on the host cores, the same cfg5 batch and metric
+    (bench_reference.batch_arm); rank 0 only."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    import bench_reference as br
     procs = os.cpu_count() or 1
-    kind = cpu_kind()
-    ctx = mp.get_context("fork")
-    rods_pp, steps_pp = 128, 10
-    vals = []
-    with ctx.Pool(procs) as pool:
-        jobs = [(rods_pp, i * rods_pp, steps_pp, kind) for i in range(procs)]
-        for _ in range(args.warmup):
-            pool.map(_cpu_worker, jobs)
-        t_all = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            out = pool.map(_cpu_worker, jobs)
-            t_all.append(time.perf_counter() - t0)
-            vals.append(sum(n / t for n, t in out))
-    value = float(np.median(vals))
-    sample = (f"hair {rods_pp} rods x {ELEMENTS} el x {steps_pp} steps per process, "
-              f"{procs} processes; element-steps/s summed over processes")
+    r = br.batch_arm(args.rods, procs, steps=args.steps, warmup=args.warmup)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value,
+        "impl": "reference", "metric": METRIC, "value": r["value"],
         "unit": "element-steps/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": float(np.median(t_all)) * 1e3,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg5 hair: 65536 rods x 128 elements (bounded CPU "
-                               "sample of the same rods)",
-                   "rods": TOTAL_RODS, "elements_per_rod": ELEMENTS,
+        "config": {"workload": "cfg5 hair: 65536 rods x 128 elements, roots clamped, "
+                               "sharded over host processes",
+                   "rods": args.rods, "elements_per_rod": ELEMENTS, "steps_per_launch": 1,
                    "iterations": 10, "dt": 1e-4},
-        "cpu_baseline": {"value": value, "unit": "element-steps/s", "cores": procs,
-                         "kind": kind, "sample": sample},
-        "e2e": {"value": value, "unit": "element-steps/s", "h2d_bytes_per_step": 0,
+        "cpu_baseline": dict(r),
+        "e2e": {"value": r["value"], "unit": "element-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -606,7 +614,8 @@ def run_ours(args):
         line["nccl_gather_elems"] = gathered
         line["state_sha256"] = digest.hexdigest()
         if world == 1 and not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(os.cpu_count() or 1)
+            import bench_reference as br
+            line["cpu_baseline"] = br.batch_arm(args.rods, os.cpu_count() or 1, steps=5, warmup=1)
         if world == 1 and not args.no_single:
             line["single_rod"] = single_rod_suite(args.precision)
         print(json.dumps(line))

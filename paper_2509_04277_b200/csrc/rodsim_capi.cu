@@ -1851,13 +1851,30 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
         int64_t pts = 0;
         for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) pts += h->h_tasks[t].np;
         static const char* names[] = {"cta", "cluster", "grid", "stream"};
-        char tmp[512];
+        // barriers per step, as the kernel issues them (rod_step.cuh): scatter,
+        // gather, integrate + per iteration the two colour phases (when any
+        // element is distance-projected or bindings are staged) and one each
+        // for contacts, self-collision pairs, bindings, grabs
+        bool binds = false, grabs = false;
+        for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
+            binds |= h->h_tasks[t].bind_count > 0;
+            grabs |= h->h_tasks[t].grab_count > 0;
+        }
+        const bool feat_k = g.tier != TIER_STREAM;
+        const int per_it = ((g.any_dist || binds) ? 2 : 0) + ((h->contacts_on && feat_k) ? 1 : 0) +
+                           ((h->d.has_self && feat_k) ? 1 : 0) + (binds ? 1 : 0) + (grabs ? 1 : 0);
+        const int64_t n_sync = 3 + h->d.iters * per_it;
+        char tmp[768];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "
                  "\"uniform\": %s, \"ctas\": %d, \"grid\": %d, \"threads\": %d, \"cluster\": %d, "
-                 "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d}",
+                 "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d, \"any_dist\": %s, "
+                 "\"bindings\": %s, \"grabs\": %s, \"contacts\": %s, \"self_collision\": %s, "
+                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld}",
                  i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni == 2 ? "\"launch\"" : (g.uni ? "true" : "false"), g.ncta,
-                 g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap);
+                 g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap, g.any_dist ? "true" : "false",
+                 binds ? "true" : "false", grabs ? "true" : "false", h->contacts_on ? "true" : "false",
+                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync);
         s += tmp;
     }
     s += std::string("], \"live\": ") + (h->live ? "true" : "false") + "}";

@@ -180,3 +180,14 @@ def test_contact_batches_stay_off_the_stream_tier():
     assert plan(w)[0]["tier"] == "stream"
     w.set_mesh(bvh.build_aabb_tree(*meshes.floor_mesh(y=-1.0, cells=2)))
     assert plan(w)[0]["tier"] == "cta"
+
+
+def test_plan_barriers_per_step():
+    # the latency roofline's n_sync: 3 + I x (2 colour phases + contacts +
+    # pairs + bindings + grabs), as the kernel issues them (rod_step.cuh)
+    assert plan(wl.cantilever())[0]["sync_per_step"] == 23      # 2I + 3
+    assert plan(wl.extensible())[0]["sync_per_step"] == 3       # no colour sweeps
+    assert plan(wl.pair())[0]["sync_per_step"] == 33            # 3I + 3
+    assert plan(wl.insertion())[0]["sync_per_step"] == 33       # + contact phase
+    assert plan(wl.knot())[0]["sync_per_step"] == 3 + 15 * 3    # + self-collision pairs
+    assert plan(wl.hair(2048))[0]["sync_per_step"] == 23
