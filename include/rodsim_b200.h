@@ -204,6 +204,10 @@ int rs_device_ptr(rs_handle h, int32_t which, void **out);
  * pairs, computed on the device with the fp64 mirror build flags. */
 int rs_selftest_div(const double *a, const double *b, int64_t n, double *q_ieee,
                     double *q_fast);
+/* Self-test: kind 0 1/a, kind 1 sqrt(a): the compiler's IEEE result and the
+ * branch-free fast-path restatement the batched kernel uses (rod_math.cuh
+ * rcp_rn / sqrt_rn), for n inputs on the device. */
+int rs_selftest_fn(int32_t kind, const double *a, int64_t n, double *r_ieee, double *r_fast);
 /* Measured issue rate of one pipe on the current device (operations/s):
  * kind 0 DFMA, 1 DADD, 2 DMUL, 3 FFMA.  Compute cross-check for the bench. */
 int rs_pipe_peak(int kind, double *ops_per_s);

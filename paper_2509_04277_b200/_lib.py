@@ -97,6 +97,7 @@ SIGNATURES = [
     ("rs_plan_json", _i32, [_p, ctypes.c_char_p, _i64]),
     ("rs_device_ptr", _i32, [_p, _i32, ctypes.POINTER(_p)]),
     ("rs_selftest_div", _i32, [_p, _p, _i64, _p, _p]),
+    ("rs_selftest_fn", _i32, [_i32, _p, _i64, _p, _p]),
     ("rs_timer_start", _i32, [_p]),
     ("rs_timer_stop", _i32, [_p]),
     ("rs_timer_ms", _f64, [_p]),

@@ -16,5 +16,8 @@ namespace RSB_MODE_NS {
 template cudaError_t launch_step<RSB_REAL>(int, int, int, const StepArgs<RSB_REAL>&, int, int, size_t, int,
                                            cudaStream_t);
 template cudaError_t occupancy<RSB_REAL>(int, int, int, int, size_t, int, int*);
+#if !RSB_FEAT
+template cudaError_t batch_step<RSB_REAL>(int, int, const StepArgs<RSB_REAL>*, int, cudaStream_t, int*);
+#endif
 }  // namespace RSB_MODE_NS
 }  // namespace rsb

@@ -8,6 +8,9 @@
 #include <atomic>
 
 #include "rod_step.cuh"
+#if !RSB_FEAT
+#include "rod_batch.cuh"
+#endif
 
 #if !defined(RSB_MODE_NS) || !defined(RSB_MODE_ID) || !defined(RSB_FEAT)
 #error "define RSB_MODE_NS, RSB_MODE_ID and RSB_FEAT before including rod_launch.cuh"
@@ -238,6 +241,45 @@ template <typename Real>
 cudaError_t occupancy(int variant, int tier, int uni, int threads, size_t smem, int cluster, int* out) {
     return dispatch<Real>(1, variant, tier, uni, nullptr, 0, threads, smem, cluster, nullptr, out);
 }
+
+
+#if !RSB_FEAT
+// The warp-per-rod batched kernel (rod_batch.cuh): launch shape `shape`
+// (kBwShapes), `grid` persistent CTAs.
+template <typename Real, int SH, bool GEN>
+static cudaError_t batch_one(int what, const StepArgs<Real>* a, int grid, cudaStream_t st, int* out) {
+    constexpr BwShape sh = kBwShapes[SH];
+    auto fn = rod_batch_kernel<Real, RSB_MODE_ID, sh.wpc, sh.minb, GEN>;
+    static std::atomic<bool> done[64];
+    cudaError_t e = configure_once(fn, done);
+    if (e != cudaSuccess) return e;
+    const size_t smem = size_t(sh.wpc) * bw_warp_bytes<Real>();
+    if (what == 1) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, 32 * sh.wpc, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32 * sh.wpc);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, *a);
+}
+
+// shape + kBwNumShapes * gen
+template <typename Real>
+cudaError_t batch_step(int what, int shape, const StepArgs<Real>* a, int grid, cudaStream_t st, int* out) {
+    switch (shape) {
+        case 0: return batch_one<Real, 0, false>(what, a, grid, st, out);
+        case 1: return batch_one<Real, 1, false>(what, a, grid, st, out);
+        case 2: return batch_one<Real, 0, true>(what, a, grid, st, out);
+        case 3: return batch_one<Real, 1, true>(what, a, grid, st, out);
+    }
+    return cudaErrorInvalidValue;
+}
+#endif
 
 }  // namespace RSB_MODE_NS
 }  // namespace rsb

@@ -319,6 +319,20 @@ __global__ void div_selftest_kernel(const double* a, const double* b, int64_t n,
         q_fast[i] = div_rn(a[i], b[i], rb);
     }
 }
+// kind 0: 1/a, kind 1: sqrt(a) -- the compiler's IEEE result and the
+// branch-free fast-path restatement (rcp_rn / sqrt_rn) the batched kernel uses
+__global__ void fn_selftest_kernel(int kind, const double* a, int64_t n, double* r_ieee, double* r_fast) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double x = a[i];
+        r_ieee[i] = kind == 0 ? 1.0 / x : sqrt(x);
+        r_fast[i] = kind == 0 ? rcp_rn(x) : sqrt_rn(x);
+    }
+}
+cudaError_t fn_selftest(int kind, const double* a, int64_t n, double* r_ieee, double* r_fast) {
+    fn_selftest_kernel<<<1184, 256>>>(kind, a, n, r_ieee, r_fast);
+    return cudaDeviceSynchronize();
+}
 cudaError_t div_selftest(const double* a, const double* b, int64_t n, double* q_ieee, double* q_fast) {
     div_selftest_kernel<<<592, 256>>>(a, b, n, q_ieee, q_fast);
     return cudaDeviceSynchronize();

@@ -24,6 +24,7 @@
 
 #include "../../include/rodsim_b200.h"
 #include "rod_common.h"
+#include "rod_batch.cuh"
 #include "rod_step.cuh"
 
 // launchers of the six kernel translation units (csrc/rod_kernels.cu)
@@ -34,6 +35,8 @@
     cudaError_t launch_step(int, int, int, const StepArgs<Real>&, int, int, size_t, int, cudaStream_t); \
     template <typename Real>                                                                       \
     cudaError_t occupancy(int, int, int, int, size_t, int, int*);                                 \
+    template <typename Real>                                                                       \
+    cudaError_t batch_step(int, int, const StepArgs<Real>*, int, cudaStream_t, int*);             \
     }                                                                                              \
     }
 RSB_DECLARE_MODE(mirror)
@@ -117,6 +120,13 @@ struct Group {       // one kernel launch
     size_t smem = 0;
     int32_t* d_flags = nullptr;   // grid tier
     void* d_halo = nullptr;
+    // stream groups of 129-point World rods: the speculative launch runs the
+    // warp-per-rod kernel (rod_batch.cuh) in launch shape bw_shape on
+    // bw_grid persistent CTAs (-1: not eligible); bw_gen: extensible
+    // elements or external forces (the general variant of the kernel)
+    int bw_shape = -1;
+    bool bw_gen = false;
+    int bw_grid = 0;
 };
 
 // groups with speculative kernels: the batched stream variant and the
@@ -154,6 +164,8 @@ struct rs_handle_s {
     int num_sms = 0;
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
     bool spec = true;               // speculative batched launches (RSB_SPEC=0: off)
+    bool bw_on = true;              // warp-per-rod batched kernel (RSB_BW=0: off)
+    int bw_shape = 0;               // its launch shape (RSB_BW_SHAPE, kBwShapes)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
 
@@ -382,6 +394,15 @@ int occupancy_query(rs_handle h, int variant, int tier, int uni, int threads, si
                      : f64fast::occupancy<double>(variant, tier, uni, threads, smem, cluster, out);
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "occupancy query failed: %s", cudaGetErrorString(e));
+    return RS_OK;
+}
+
+int batch_occupancy(rs_handle h, int shape, int* out) {
+    cudaError_t e;
+    if (h->prec == RS_F64_MIRROR) e = mirror::batch_step<double>(1, shape, nullptr, 0, nullptr, out);
+    else if (h->prec == RS_F32) e = f32::batch_step<float>(1, shape, nullptr, 0, nullptr, out);
+    else e = f64fast::batch_step<double>(1, shape, nullptr, 0, nullptr, out);
+    if (e != cudaSuccess) return fail(RS_E_CUDA, "batch kernel occupancy query failed: %s", cudaGetErrorString(e));
     return RS_OK;
 }
 
@@ -766,6 +787,30 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                 single = h->h_tasks[t].nrods == 1 && h->h_tasks[t].bind_count == 0;
             if (single) g.tier = TIER_STREAM;
         }
+        // warp-per-rod batched kernel: every task one 129-point rod whose
+        // flags are the structural ones of a World rod (elements, junctions
+        // and colours by local index; no drivers), launch-uniform constants
+        if (g.tier == TIER_STREAM && g.variant == kBatchVariant && g.uni == 2 && h->bw_on) {
+            bool ok = true;
+            for (int t = g.task_begin; t < g.task_begin + g.ncta && ok; ++t) {
+                const CtaTask& tk = h->h_tasks[t];
+                ok = tk.np == BW_NP && tk.nrods == 1 && tk.drv_count == 0 && tk.bind_count == 0;
+                for (int j = 0; j < BW_NP && ok; ++j) {
+                    const uint32_t f = pflags[tk.p0 + j];
+                    const uint32_t want = (j < BW_NE ? uint32_t(SF_HAS_ELEM) : 0u) | (j > 0 ? uint32_t(SF_HAS_PREV) : 0u) |
+                                          (j < BW_NE - 1 ? uint32_t(SF_JVALID) : 0u) |
+                                          (j > 0 && j < BW_NE ? uint32_t(SF_JPREV) : 0u) |
+                                          (j < BW_NE && (j & 1) ? uint32_t(SF_PARITY) : 0u);
+                    const uint32_t mask = SF_HAS_ELEM | SF_HAS_PREV | SF_JVALID | SF_JPREV | SF_PARITY | SF_DRV_PT | SF_DRV_FR;
+                    ok = (f & mask) == want && pt_elem[tk.p0 + j] == (j < BW_NE ? tk.e0 + j : -1);
+                }
+            }
+            g.bw_shape = ok ? h->bw_shape : -1;
+            bool gen = false;   // (external forces are checked at launch: h->has_fext)
+            for (int t = g.task_begin; t < g.task_begin + g.ncta && ok && !gen; ++t)
+                for (int j = 0; j < BW_NE && !gen; ++j) gen = (pflags[h->h_tasks[t].p0 + j] & SF_EXT) != 0;
+            g.bw_gen = gen;
+        }
         const bool stream = g.tier == TIER_STREAM && stream_staged(var.S, var.CAP);
         size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap, stream).total
                                         : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap, stream).total;
@@ -804,6 +849,19 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             int per_sm = occ;
             if (const char* e = getenv("RSB_STREAM_CTAS")) per_sm = std::max(1, std::min(occ, atoi(e)));
             g.grid = std::min(g.ncta, per_sm * h->num_sms);
+        }
+        if (g.bw_shape >= 0) {
+            int bocc = 0, bocc_gen = 0;   // both kernel variants: fext may appear later
+            int rcb = batch_occupancy(h, g.bw_shape, &bocc);
+            if (!rcb) rcb = batch_occupancy(h, g.bw_shape + kBwNumShapes, &bocc_gen);
+            if (rcb) return rcb;
+            bocc = std::min(bocc, bocc_gen);
+            if (bocc < 1) {
+                g.bw_shape = -1;
+            } else {
+                const int wpc = kBwShapes[g.bw_shape].wpc;
+                g.bw_grid = std::min((g.ncta + wpc - 1) / wpc, bocc * h->num_sms);
+            }
         }
         if (spec_group(g) && !h->dry) {   // the speculative launch's redo list
             int rc2 = dev_alloc(h->redo_list, sizeof(int32_t) * size_t(g.ncta));
@@ -1263,7 +1321,31 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         return feat ? f64fast_feat::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st)
                     : f64fast::launch_step<double>(g.variant, g.tier, cfg, a, grid, g.threads, g.smem, g.cluster, h->st);
     };
-    cudaError_t e = spec ? one(cfg0 + 6, 0) : one(cfg0, 0);
+    // the warp-per-rod kernel takes the speculative launch of an eligible
+    // group when no grab is active (grab anchors run on the general kernel)
+    const bool bw = spec && g.bw_shape >= 0 && h->h_grabs.empty();
+    auto one_bw = [&]() -> cudaError_t {
+        const int bsel = g.bw_shape + ((g.bw_gen || h->has_fext) ? kBwNumShapes : 0);
+        const int bgrid = t_cnt < 0 ? g.bw_grid : std::min(g.bw_grid, (nt + kBwShapes[g.bw_shape].wpc - 1) / kBwShapes[g.bw_shape].wpc);
+        auto go = [&](auto a) {
+            a.tasks += t_off;
+            a.ntasks = nt;
+            a.redo_list = static_cast<int32_t*>(h->redo_list.p);
+            a.redo_count = static_cast<int32_t*>(h->redo_count.p);
+            a.redo_mode = 0;
+            return a;
+        };
+        if (h->prec == RS_F64_MIRROR) {
+            auto a = go(make_args<double>(h, g, step0, steps));
+            return mirror::batch_step<double>(0, bsel, &a, bgrid, h->st, nullptr);
+        } else if (h->prec == RS_F32) {
+            auto a = go(make_args<float>(h, g, step0, steps));
+            return f32::batch_step<float>(0, bsel, &a, bgrid, h->st, nullptr);
+        }
+        auto a = go(make_args<double>(h, g, step0, steps));
+        return f64fast::batch_step<double>(0, bsel, &a, bgrid, h->st, nullptr);
+    };
+    cudaError_t e = bw ? one_bw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
     if (e == cudaSuccess && spec) e = one(cfg0, 1);
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
@@ -1430,6 +1512,8 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     h->step = desc->step_index;
     if (const char* dbg = getenv("RSB_DEBUG")) h->debug = atoi(dbg);
     if (const char* sp = getenv("RSB_SPEC")) h->spec = atoi(sp) != 0;
+    if (const char* sp = getenv("RSB_BW")) h->bw_on = atoi(sp) != 0;
+    if (const char* sp = getenv("RSB_BW_SHAPE")) h->bw_shape = std::max(0, std::min(kBwNumShapes - 1, atoi(sp)));
     if (cudaHostAlloc(reinterpret_cast<void**>(&h->ring), sizeof(LiveRing), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->ring_dev), h->ring, 0) != cudaSuccess) {
         cudaGetLastError();
@@ -1914,6 +1998,7 @@ int rs_device_ptr(rs_handle h, int32_t which, void** out) {
 namespace rsb {
 namespace micro {   // csrc/rod_micro.cu
 cudaError_t div_selftest(const double*, const double*, int64_t, double*, double*);
+cudaError_t fn_selftest(int, const double*, int64_t, double*, double*);
 cudaError_t pipe_peak(int kind, int blocks, int threads, int iters, float* ms, double* ops);
 }  // namespace micro
 }  // namespace rsb
@@ -1926,6 +2011,23 @@ extern "C" int rs_pipe_peak(int kind, double* ops_per_s) {
     double ops = 0.0;
     CK(rsb::micro::pipe_peak(kind, sms * 8, 256, 4096, &ms, &ops));
     *ops_per_s = ops / (double(ms) * 1e-3);
+    return RS_OK;
+}
+
+extern "C" int rs_selftest_fn(int32_t kind, const double* a, int64_t n, double* r_ieee, double* r_fast) {
+    if (kind < 0 || kind > 1 || n < 0) return fail(RS_E_INVALID, "bad argument");
+    double *da = nullptr, *dr = nullptr, *df = nullptr;
+    const size_t bytes = sizeof(double) * size_t(std::max<int64_t>(n, 1));
+    CK(cudaMalloc(&da, bytes));
+    CK(cudaMalloc(&dr, bytes));
+    CK(cudaMalloc(&df, bytes));
+    CK(cudaMemcpy(da, a, sizeof(double) * size_t(n), cudaMemcpyHostToDevice));
+    CK(rsb::micro::fn_selftest(kind, da, n, dr, df));
+    CK(cudaMemcpy(r_ieee, dr, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r_fast, df, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost));
+    cudaFree(da);
+    cudaFree(dr);
+    cudaFree(df);
     return RS_OK;
 }
 
