@@ -274,8 +274,10 @@ cudaError_t batch_step(int what, int shape, const StepArgs<Real>* a, int grid, c
     switch (shape) {
         case 0: return batch_one<Real, 0, false>(what, a, grid, st, out);
         case 1: return batch_one<Real, 1, false>(what, a, grid, st, out);
-        case 2: return batch_one<Real, 0, true>(what, a, grid, st, out);
-        case 3: return batch_one<Real, 1, true>(what, a, grid, st, out);
+        case 2: return batch_one<Real, 2, false>(what, a, grid, st, out);
+        case 3: return batch_one<Real, 0, true>(what, a, grid, st, out);
+        case 4: return batch_one<Real, 1, true>(what, a, grid, st, out);
+        case 5: return batch_one<Real, 2, true>(what, a, grid, st, out);
     }
     return cudaErrorInvalidValue;
 }

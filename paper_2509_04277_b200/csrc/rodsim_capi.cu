@@ -165,7 +165,7 @@ struct rs_handle_s {
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
     bool spec = true;               // speculative batched launches (RSB_SPEC=0: off)
     bool bw_on = true;              // warp-per-rod batched kernel (RSB_BW=0: off)
-    int bw_shape = 0;               // its launch shape (RSB_BW_SHAPE, kBwShapes)
+    int bw_shape = 1;               // its launch shape (RSB_BW_SHAPE, kBwShapes)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
 
@@ -1948,17 +1948,23 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
         const int per_it = ((g.any_dist || binds) ? 2 : 0) + ((h->contacts_on && feat_k) ? 1 : 0) +
                            ((h->d.has_self && feat_k) ? 1 : 0) + (binds ? 1 : 0) + (grabs ? 1 : 0);
         const int64_t n_sync = 3 + h->d.iters * per_it;
-        char tmp[768];
+        // the warp-per-rod kernel (rod_batch.cuh) that takes the group's
+        // speculative launches: shape (warps per CTA), persistent CTAs
+        char bwj[96] = "null";
+        if (g.bw_shape >= 0)
+            snprintf(bwj, sizeof bwj, "{\"warps_per_cta\": %d, \"grid\": %d, \"general\": %s}",
+                     kBwShapes[g.bw_shape].wpc, g.bw_grid, g.bw_gen ? "true" : "false");
+        char tmp[900];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "
                  "\"uniform\": %s, \"ctas\": %d, \"grid\": %d, \"threads\": %d, \"cluster\": %d, "
                  "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d, \"any_dist\": %s, "
                  "\"bindings\": %s, \"grabs\": %s, \"contacts\": %s, \"self_collision\": %s, "
-                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld}",
+                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld, \"warp_per_rod\": %s}",
                  i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni == 2 ? "\"launch\"" : (g.uni ? "true" : "false"), g.ncta,
                  g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap, g.any_dist ? "true" : "false",
                  binds ? "true" : "false", grabs ? "true" : "false", h->contacts_on ? "true" : "false",
-                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync);
+                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync, bwj);
         s += tmp;
     }
     s += std::string("], \"live\": ") + (h->live ? "true" : "false") + "}";

@@ -371,30 +371,45 @@ def test_fp64_fast_mode_within_1e9():
 
 @pytest.mark.parametrize("precision", ["f32", "f64_fast"])
 def test_batched_stream_tier_reduced_precision(precision, monkeypatch):
-    # the speculative batched launches in the fp32 and fast fp64 modes give
-    # the same bits as the exact kernel (RSB_SPEC=0), and stay near the
-    # oracle: fast fp64 within 1e-9 relative; fp32 within 1e-3 L at every
-    # point after 200 steps (1700 randomly oriented rods: a few are
-    # sensitive enough that fp32 drifts past the 1e-5 L stated for the
-    # 8-rod sample, with or without speculation) and 1e-4 L for 99.9 %
-    runs = {}
+    # the speculative batched launches (the warp-per-rod kernel) and the
+    # general exact kernel (RSB_SPEC=0) in the fp32 and fast fp64 modes both
+    # stay near the oracle: fast fp64 within 1e-9 relative; fp32 within
+    # 1e-3 L at every point after 200 steps (1700 randomly oriented rods: a
+    # few are sensitive enough that fp32 drifts past the 1e-5 L stated for
+    # the 8-rod sample, with or without speculation) and 1e-4 L for 99.9 %.
+    # (The fast modes contract multiply-adds, so two different kernels need
+    # not agree bit for bit there; the fp64 mirror mode does, see below.)
+    r = wl.hair(1700)
+    OracleStepper(r).run(200)
+    L = 128 * float(np.mean(r.rest_lengths))
     for spec in ("1", "0"):
         monkeypatch.setenv("RSB_SPEC", spec)
         g = wl.hair(1700)
         plan = run_gpu(g, 200, 50, precision=precision)
-        assert plan["groups"][0]["tier"] == "stream" and plan["groups"][0]["variant"] == 7
-        runs[spec] = g
-    for a in ("positions", "velocities", "frames", "angular_velocities"):
-        assert np.array_equal(getattr(runs["1"], a).view(np.int64), getattr(runs["0"], a).view(np.int64)), a
-    r = wl.hair(1700)
-    OracleStepper(r).run(200)
-    g = runs["1"]
-    dr = np.abs(g.positions - r.positions).max(axis=1)
-    if precision == "f64_fast":
-        assert dr.max() <= 1e-9 * np.abs(r.positions).max()
-    else:
-        L = 128 * float(np.mean(r.rest_lengths))
-        assert dr.max() <= 1e-3 * L and np.quantile(dr, 0.999) <= 1e-4 * L
+        grp = plan["groups"][0]
+        assert grp["tier"] == "stream" and grp["variant"] == 7
+        dr = np.abs(g.positions - r.positions).max(axis=1)
+        if precision == "f64_fast":
+            assert dr.max() <= 1e-9 * np.abs(r.positions).max(), spec
+        else:
+            assert dr.max() <= 1e-3 * L and np.quantile(dr, 0.999) <= 1e-4 * L, spec
+
+
+def test_warp_per_rod_kernel_bitwise_with_general(monkeypatch):
+    # fp64 mirror: the warp-per-rod batched kernel (rod_batch.cuh) and the
+    # general stream kernel it replaces give the same bits, every shape
+    g0 = wl.hair(3000)
+    monkeypatch.setenv("RSB_BW", "0")
+    plan = run_gpu(g0, 60, 1)
+    assert plan["groups"][0]["warp_per_rod"] is None
+    for shape in ("0", "1", "2"):
+        monkeypatch.setenv("RSB_BW", "1")
+        monkeypatch.setenv("RSB_BW_SHAPE", shape)
+        g = wl.hair(3000)
+        plan = run_gpu(g, 60, 1)
+        assert plan["groups"][0]["warp_per_rod"] is not None
+        for a in ("positions", "velocities", "frames", "angular_velocities"):
+            assert np.array_equal(getattr(g, a).view(np.int64), getattr(g0, a).view(np.int64)), (shape, a)
 
 
 @pytest.mark.parametrize("lo,tier", [(66, "stream"), (2, "cta")])
