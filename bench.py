@@ -77,10 +77,10 @@ def load_peaks():
 
 # fp64 pipe instructions the fp64 mirror kernel issues per slot-step (ncu
 # smsp__sass_thread_inst_executed_op_{dadd,dmul,dfma}_pred_on of the
-# speculative variant-7 kernel, profiles/r01g_ncu_full_hair.json capture:
-# 5.79e9 per launch / 8.45e6 slots; the exact kernel issues 666): the
-# compute cross-check
-FP64_INST_PER_SLOT_STEP = 685
+# warp-per-rod batched kernel, profiles/r02n_ncu_full_warp_kernel.json
+# capture: 5.85e9 per launch / 8.45e6 slots; the general variant-7 kernel
+# issued 685): the compute cross-check
+FP64_INST_PER_SLOT_STEP = 692
 
 
 def fp64_peak():
