@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "rod_step.cuh"
 #if !RSB_FEAT
@@ -249,11 +250,17 @@ cudaError_t occupancy(int variant, int tier, int uni, int threads, size_t smem, 
 template <typename Real, int SH, bool GEN>
 static cudaError_t batch_one(int what, const StepArgs<Real>* a, int grid, cudaStream_t st, int* out) {
     constexpr BwShape sh = kBwShapes[SH];
-    auto fn = rod_batch_kernel<Real, RSB_MODE_ID, sh.wpc, sh.minb, GEN>;
+    auto fn = rod_batch_kernel<Real, RSB_MODE_ID, sh.wpc, sh.minb, GEN, sh.shst>;
     static std::atomic<bool> done[64];
     cudaError_t e = configure_once(fn, done);
     if (e != cudaSuccess) return e;
-    const size_t smem = size_t(sh.wpc) * bw_warp_bytes<Real>();
+    // RSB_BW_PAD (bytes, tuning experiments): extra shared memory per CTA,
+    // i.e. fewer resident CTAs per SM
+    static const size_t pad = [] {
+        const char* e = getenv("RSB_BW_PAD");
+        return e ? size_t(atol(e)) : size_t(0);
+    }();
+    const size_t smem = bw_smem_bytes<Real>(sh.wpc, sh.shst) + pad;
     if (what == 1) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, 32 * sh.wpc, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -268,16 +275,16 @@ static cudaError_t batch_one(int what, const StepArgs<Real>* a, int grid, cudaSt
     return cudaLaunchKernelEx(&cfg, fn, *a);
 }
 
-// shape + kBwNumShapes * gen
+// shape in [0, kBwNumShapes) with gen = false, or kBwNumShapes + shape for
+// the GEN kernel (extensible elements / external forces: kBwGenShape only)
 template <typename Real>
-cudaError_t batch_step(int what, int shape, const StepArgs<Real>* a, int grid, cudaStream_t st, int* out) {
-    switch (shape) {
+cudaError_t batch_step(int what, int sel, const StepArgs<Real>* a, int grid, cudaStream_t st, int* out) {
+    switch (sel) {
         case 0: return batch_one<Real, 0, false>(what, a, grid, st, out);
         case 1: return batch_one<Real, 1, false>(what, a, grid, st, out);
         case 2: return batch_one<Real, 2, false>(what, a, grid, st, out);
-        case 3: return batch_one<Real, 0, true>(what, a, grid, st, out);
-        case 4: return batch_one<Real, 1, true>(what, a, grid, st, out);
-        case 5: return batch_one<Real, 2, true>(what, a, grid, st, out);
+        case 3: return batch_one<Real, 3, false>(what, a, grid, st, out);
+        case kBwNumShapes + kBwGenShape: return batch_one<Real, kBwGenShape, true>(what, a, grid, st, out);
     }
     return cudaErrorInvalidValue;
 }

@@ -123,9 +123,11 @@ struct Group {       // one kernel launch
     // stream groups of 129-point World rods: the speculative launch runs the
     // warp-per-rod kernel (rod_batch.cuh) in launch shape bw_shape on
     // bw_grid persistent CTAs (-1: not eligible); bw_gen: extensible
-    // elements or external forces (the general variant of the kernel)
+    // elements (the general variant of the kernel, shape kBwGenShape on
+    // bw_grid_gen CTAs -- also taken when external forces appear)
     int bw_shape = -1;
     bool bw_gen = false;
+    int bw_grid_gen = 0;
     int bw_grid = 0;
 };
 
@@ -165,7 +167,7 @@ struct rs_handle_s {
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
     bool spec = true;               // speculative batched launches (RSB_SPEC=0: off)
     bool bw_on = true;              // warp-per-rod batched kernel (RSB_BW=0: off)
-    int bw_shape = 1;               // its launch shape (RSB_BW_SHAPE, kBwShapes)
+    int bw_shape = -1;              // its launch shape (RSB_BW_SHAPE, kBwShapes; -1: the planner's)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
 
@@ -805,11 +807,22 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                     ok = (f & mask) == want && pt_elem[tk.p0 + j] == (j < BW_NE ? tk.e0 + j : -1);
                 }
             }
-            g.bw_shape = ok ? h->bw_shape : -1;
             bool gen = false;   // (external forces are checked at launch: h->has_fext)
             for (int t = g.task_begin; t < g.task_begin + g.ncta && ok && !gen; ++t)
                 for (int j = 0; j < BW_NE && !gen; ++j) gen = (pflags[h->h_tasks[t].p0 + j] & SF_EXT) != 0;
             g.bw_gen = gen;
+            // rods sharing their mass and inverse-mass arrays bit for bit:
+            // the statics live once per CTA (more warps per SM)
+            bool shared = ok;
+            const int64_t q0 = h->h_tasks[g.task_begin].p0;
+            for (int t = g.task_begin + 1; t < g.task_begin + g.ncta && shared; ++t) {
+                const int64_t p = h->h_tasks[t].p0;
+                shared = std::memcmp(d.mass + p, d.mass + q0, sizeof(double) * BW_NP) == 0 &&
+                         std::memcmp(d.invm + p, d.invm + q0, sizeof(double) * BW_NP) == 0;
+            }
+            int shape = h->bw_shape >= 0 ? h->bw_shape : 1;
+            if (kBwShapes[shape].shst && !shared) shape = 1;
+            g.bw_shape = ok ? shape : -1;
         }
         const bool stream = g.tier == TIER_STREAM && stream_staged(var.S, var.CAP);
         size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap, stream).total
@@ -851,16 +864,16 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             g.grid = std::min(g.ncta, per_sm * h->num_sms);
         }
         if (g.bw_shape >= 0) {
-            int bocc = 0, bocc_gen = 0;   // both kernel variants: fext may appear later
+            int bocc = 0, bocc_gen = 0;   // both kernels: external forces may appear later
             int rcb = batch_occupancy(h, g.bw_shape, &bocc);
-            if (!rcb) rcb = batch_occupancy(h, g.bw_shape + kBwNumShapes, &bocc_gen);
+            if (!rcb) rcb = batch_occupancy(h, kBwNumShapes + kBwGenShape, &bocc_gen);
             if (rcb) return rcb;
-            bocc = std::min(bocc, bocc_gen);
-            if (bocc < 1) {
+            if (bocc < 1 || bocc_gen < 1) {
                 g.bw_shape = -1;
             } else {
-                const int wpc = kBwShapes[g.bw_shape].wpc;
+                const int wpc = kBwShapes[g.bw_shape].wpc, wpg = kBwShapes[kBwGenShape].wpc;
                 g.bw_grid = std::min((g.ncta + wpc - 1) / wpc, bocc * h->num_sms);
+                g.bw_grid_gen = std::min((g.ncta + wpg - 1) / wpg, bocc_gen * h->num_sms);
             }
         }
         if (spec_group(g) && !h->dry) {   // the speculative launch's redo list
@@ -1325,8 +1338,11 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // group when no grab is active (grab anchors run on the general kernel)
     const bool bw = spec && g.bw_shape >= 0 && h->h_grabs.empty();
     auto one_bw = [&]() -> cudaError_t {
-        const int bsel = g.bw_shape + ((g.bw_gen || h->has_fext) ? kBwNumShapes : 0);
-        const int bgrid = t_cnt < 0 ? g.bw_grid : std::min(g.bw_grid, (nt + kBwShapes[g.bw_shape].wpc - 1) / kBwShapes[g.bw_shape].wpc);
+        const bool gen = g.bw_gen || h->has_fext;
+        const int bsel = gen ? kBwNumShapes + kBwGenShape : g.bw_shape;
+        const int wpc = kBwShapes[gen ? kBwGenShape : g.bw_shape].wpc;
+        const int full = gen ? g.bw_grid_gen : g.bw_grid;
+        const int bgrid = t_cnt < 0 ? full : std::min(full, (nt + wpc - 1) / wpc);
         auto go = [&](auto a) {
             a.tasks += t_off;
             a.ntasks = nt;
@@ -1950,10 +1966,11 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
         const int64_t n_sync = 3 + h->d.iters * per_it;
         // the warp-per-rod kernel (rod_batch.cuh) that takes the group's
         // speculative launches: shape (warps per CTA), persistent CTAs
-        char bwj[96] = "null";
+        char bwj[160] = "null";
         if (g.bw_shape >= 0)
-            snprintf(bwj, sizeof bwj, "{\"warps_per_cta\": %d, \"grid\": %d, \"general\": %s}",
-                     kBwShapes[g.bw_shape].wpc, g.bw_grid, g.bw_gen ? "true" : "false");
+            snprintf(bwj, sizeof bwj, "{\"shape\": %d, \"warps_per_cta\": %d, \"grid\": %d, \"shared_statics\": %s, \"general\": %s}",
+                     g.bw_shape, kBwShapes[g.bw_shape].wpc, g.bw_grid, kBwShapes[g.bw_shape].shst ? "true" : "false",
+                     g.bw_gen ? "true" : "false");
         char tmp[900];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "

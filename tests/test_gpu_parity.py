@@ -402,7 +402,7 @@ def test_warp_per_rod_kernel_bitwise_with_general(monkeypatch):
     monkeypatch.setenv("RSB_BW", "0")
     plan = run_gpu(g0, 60, 1)
     assert plan["groups"][0]["warp_per_rod"] is None
-    for shape in ("0", "1", "2"):
+    for shape in ("0", "1", "2", "3"):
         monkeypatch.setenv("RSB_BW", "1")
         monkeypatch.setenv("RSB_BW_SHAPE", shape)
         g = wl.hair(3000)
