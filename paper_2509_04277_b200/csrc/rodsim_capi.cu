@@ -820,7 +820,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                 shared = std::memcmp(d.mass + p, d.mass + q0, sizeof(double) * BW_NP) == 0 &&
                          std::memcmp(d.invm + p, d.invm + q0, sizeof(double) * BW_NP) == 0;
             }
-            int shape = h->bw_shape >= 0 ? h->bw_shape : 1;
+            int shape = h->bw_shape >= 0 ? h->bw_shape : (shared ? 3 : 1);
             if (kBwShapes[shape].shst && !shared) shape = 1;
             g.bw_shape = ok ? shape : -1;
         }
