@@ -11,6 +11,7 @@
 #include "rod_step.cuh"
 #if !RSB_FEAT
 #include "rod_batch.cuh"
+#include "rod_warp.cuh"
 #endif
 
 #if !defined(RSB_MODE_NS) || !defined(RSB_MODE_ID) || !defined(RSB_FEAT)
@@ -273,6 +274,32 @@ static cudaError_t batch_one(int what, const StepArgs<Real>* a, int grid, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fn, *a);
+}
+
+// The one-warp single-rod kernel (rod_warp.cuh): one warp per task.
+template <typename Real, bool GEN, int FORM>
+static cudaError_t warp_one(const StepArgs<Real>* a, int grid, cudaStream_t st) {
+    auto fn = FORM == 1 ? rod_warp1_kernel<Real, RSB_MODE_ID, GEN> : rod_warp_kernel<Real, RSB_MODE_ID, GEN>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, *a);
+}
+// form 1: one point per lane (rods <= 31 elements); 2: two per lane (32..63)
+template <typename Real>
+cudaError_t warp_step(int gen, int form, const StepArgs<Real>* a, int grid, cudaStream_t st) {
+    switch (form) {
+        case 1: return gen ? warp_one<Real, true, 1>(a, grid, st) : warp_one<Real, false, 1>(a, grid, st);
+        case 2: return gen ? warp_one<Real, true, 2>(a, grid, st) : warp_one<Real, false, 2>(a, grid, st);
+    }
+    return cudaErrorInvalidValue;
 }
 
 // shape in [0, kBwNumShapes) with gen = false, or kBwNumShapes + shape for

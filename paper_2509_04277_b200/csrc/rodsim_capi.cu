@@ -25,6 +25,7 @@
 #include "../../include/rodsim_b200.h"
 #include "rod_common.h"
 #include "rod_batch.cuh"
+#include "rod_warp.cuh"
 #include "rod_step.cuh"
 
 // launchers of the six kernel translation units (csrc/rod_kernels.cu)
@@ -37,6 +38,8 @@
     cudaError_t occupancy(int, int, int, int, size_t, int, int*);                                 \
     template <typename Real>                                                                       \
     cudaError_t batch_step(int, int, const StepArgs<Real>*, int, cudaStream_t, int*);             \
+    template <typename Real>                                                                       \
+    cudaError_t warp_step(int, int, const StepArgs<Real>*, int, cudaStream_t);                    \
     }                                                                                              \
     }
 RSB_DECLARE_MODE(mirror)
@@ -128,6 +131,12 @@ struct Group {       // one kernel launch
     int bw_shape = -1;
     bool bw_gen = false;
     int bw_grid_gen = 0;
+    // CTA-tier groups of single rods of <= 64 elements: the speculative
+    // launch runs the one-warp register-resident kernel (rod_warp.cuh)
+    bool rw = false;
+    bool rw_gen = false;            // ... with extensible elements (GEN kernel)
+    int rw_form = 0;                // 1: every rod <= 31 elements (one point per lane),
+                                    // 2: 32..63 (two per lane)
     int bw_grid = 0;
 };
 
@@ -167,6 +176,8 @@ struct rs_handle_s {
     int debug = 0;                  // RSB_DEBUG env: bit 0 poisons smem
     bool spec = true;               // speculative batched launches (RSB_SPEC=0: off)
     bool bw_on = true;              // warp-per-rod batched kernel (RSB_BW=0: off)
+    bool rw_on = true;              // one-warp single-rod kernel (RSB_RW=0: off)
+    bool rw1_on = true;             // its one-point-per-lane form (RSB_RW1=0: off)
     int bw_shape = -1;              // its launch shape (RSB_BW_SHAPE, kBwShapes; -1: the planner's)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
@@ -824,6 +835,39 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             if (kBwShapes[shape].shst && !shared) shape = 1;
             g.bw_shape = ok ? shape : -1;
         }
+        // one-warp kernel: every task one rod of <= 64 elements with the
+        // structural flags of a World rod, launch-uniform constants
+        g.rw = false;
+        if (g.tier == TIER_CTA && g.variant == 0 && g.uni == 2 && h->rw_on && !h->contacts_on && !d.has_self &&
+            !d.live) {
+            bool ok = true;
+            for (int t = g.task_begin; t < g.task_begin + g.ncta && ok; ++t) {
+                const CtaTask& tk = h->h_tasks[t];
+                const int ne = tk.np - 1;
+                ok = tk.nrods == 1 && ne >= 1 && ne <= RW_MAX_EL && tk.drv_count == 0 && tk.bind_count == 0;
+                for (int j = 0; j <= ne && ok; ++j) {
+                    const uint32_t f = pflags[tk.p0 + j];
+                    const uint32_t want = (j < ne ? uint32_t(SF_HAS_ELEM) : 0u) | (j > 0 ? uint32_t(SF_HAS_PREV) : 0u) |
+                                          (j < ne - 1 ? uint32_t(SF_JVALID) : 0u) |
+                                          (j > 0 && j < ne ? uint32_t(SF_JPREV) : 0u) |
+                                          (j < ne && (j & 1) ? uint32_t(SF_PARITY) : 0u);
+                    const uint32_t mask = SF_HAS_ELEM | SF_HAS_PREV | SF_JVALID | SF_JPREV | SF_PARITY | SF_DRV_PT | SF_DRV_FR;
+                    ok = (f & mask) == want && pt_elem[tk.p0 + j] == (j < ne ? tk.e0 + j : -1);
+                }
+            }
+            int ne_min = 1 << 30, ne_max = 0;
+            for (int t = g.task_begin; t < g.task_begin + g.ncta; ++t) {
+                ne_min = std::min(ne_min, h->h_tasks[t].np - 1);
+                ne_max = std::max(ne_max, h->h_tasks[t].np - 1);
+            }
+            g.rw_form = (ne_max <= RW1_MAX_EL && h->rw1_on) ? 1 : (ne_max <= RW_MAX_EL ? 2 : 0);
+            (void)ne_min;
+            g.rw = ok && g.rw_form > 0;
+            g.rw_gen = false;
+            for (int t = g.task_begin; t < g.task_begin + g.ncta && ok && !g.rw_gen; ++t)
+                for (int j = 0; j < h->h_tasks[t].np - 1 && !g.rw_gen; ++j)
+                    g.rw_gen = (pflags[h->h_tasks[t].p0 + j] & SF_EXT) != 0;
+        }
         const bool stream = g.tier == TIER_STREAM && stream_staged(var.S, var.CAP);
         size_t smem = h->prec == RS_F32 ? SmemLayout<float>(var.CAP, g.bind_cap, g.drv_cap, stream).total
                                         : SmemLayout<double>(var.CAP, g.bind_cap, g.drv_cap, stream).total;
@@ -1361,7 +1405,28 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         auto a = go(make_args<double>(h, g, step0, steps));
         return f64fast::batch_step<double>(0, bsel, &a, bgrid, h->st, nullptr);
     };
-    cudaError_t e = bw ? one_bw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
+    const bool rw = spec && g.rw && h->h_grabs.empty() && !h->live;
+    auto one_rw = [&]() -> cudaError_t {
+        const int gen = (h->has_fext || g.rw_gen) ? 1 : 0;
+        auto go = [&](auto a) {
+            a.tasks += t_off;
+            a.ntasks = nt;
+            a.redo_list = static_cast<int32_t*>(h->redo_list.p);
+            a.redo_count = static_cast<int32_t*>(h->redo_count.p);
+            a.redo_mode = 0;
+            return a;
+        };
+        if (h->prec == RS_F64_MIRROR) {
+            auto a = go(make_args<double>(h, g, step0, steps));
+            return mirror::warp_step<double>(gen, g.rw_form, &a, nt, h->st);
+        } else if (h->prec == RS_F32) {
+            auto a = go(make_args<float>(h, g, step0, steps));
+            return f32::warp_step<float>(gen, g.rw_form, &a, nt, h->st);
+        }
+        auto a = go(make_args<double>(h, g, step0, steps));
+        return f64fast::warp_step<double>(gen, g.rw_form, &a, nt, h->st);
+    };
+    cudaError_t e = bw ? one_bw() : rw ? one_rw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
     if (e == cudaSuccess && spec) e = one(cfg0, 1);
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
@@ -1529,6 +1594,8 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     if (const char* dbg = getenv("RSB_DEBUG")) h->debug = atoi(dbg);
     if (const char* sp = getenv("RSB_SPEC")) h->spec = atoi(sp) != 0;
     if (const char* sp = getenv("RSB_BW")) h->bw_on = atoi(sp) != 0;
+    if (const char* sp = getenv("RSB_RW")) h->rw_on = atoi(sp) != 0;
+    if (const char* sp = getenv("RSB_RW1")) h->rw1_on = atoi(sp) != 0;
     if (const char* sp = getenv("RSB_BW_SHAPE")) h->bw_shape = std::max(0, std::min(kBwNumShapes - 1, atoi(sp)));
     if (cudaHostAlloc(reinterpret_cast<void**>(&h->ring), sizeof(LiveRing), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->ring_dev), h->ring, 0) != cudaSuccess) {
@@ -1977,11 +2044,11 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
                  "\"uniform\": %s, \"ctas\": %d, \"grid\": %d, \"threads\": %d, \"cluster\": %d, "
                  "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d, \"any_dist\": %s, "
                  "\"bindings\": %s, \"grabs\": %s, \"contacts\": %s, \"self_collision\": %s, "
-                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld, \"warp_per_rod\": %s}",
+                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld, \"warp_per_rod\": %s, \"one_warp_rod\": %s}",
                  i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni == 2 ? "\"launch\"" : (g.uni ? "true" : "false"), g.ncta,
                  g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap, g.any_dist ? "true" : "false",
                  binds ? "true" : "false", grabs ? "true" : "false", h->contacts_on ? "true" : "false",
-                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync, bwj);
+                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync, bwj, g.rw ? (g.rw_form == 1 ? "\"point_per_lane\"" : "\"two_per_lane\"") : "false");
         s += tmp;
     }
     s += std::string("], \"live\": ") + (h->live ? "true" : "false") + "}";

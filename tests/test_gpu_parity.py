@@ -557,3 +557,51 @@ def test_parallel_backend_reports_barrier_waits_bitwise(make, k):
     assert all(w > 0 for w in waits), waits
     # at most the whole epoch's wall time per CTA
     assert max(waits) < 1e9
+
+
+# -- one-warp register-resident kernels for single short rods -----------------
+# (rod_warp1.cuh: one point per lane, <= 31 elements; rod_warp.cuh: two per
+# lane, 32..63) -- the speculative launch of a single-rod CTA group in epochs
+# of >= 32 steps
+
+@pytest.mark.parametrize("n", [1, 2, 7, 16, 31, 32, 33, 48, 63])
+def test_one_warp_kernel_bitwise(n):
+    g = parity(lambda: wl.sweep(n), 300, 100)
+    with Engine(wl.sweep(n)) as eng:
+        grp = eng.plan()["groups"][0]
+    assert grp["one_warp_rod"] == ("point_per_lane" if n <= 31 else "two_per_lane"), grp
+    assert np.isfinite(g.positions).all()
+
+
+@pytest.mark.parametrize("n", [24, 40])
+def test_one_warp_kernel_locks(n):
+    # a point clamped mid-rod and a locked frame besides the clamped root,
+    # tilted rod, epochs of 64 steps
+    def make():
+        w = World(dt=1e-4, gravity=(0.0, -9.81, 0.0), solver=SolverConfig(iterations=10))
+        w.add_rod(st.init_rod(n + 1, 2e-3 * n, axis=(1.0, 0.2, 0.1)), st.RodParams(**wl.MATERIAL))
+        w.finalize()
+        w.clamp_point(0, 0)
+        w.clamp_point(0, n // 2)
+        w.clamp_frame(0, n // 3)
+        return w
+    parity(make, 192, 64)
+    with Engine(make()) as eng:
+        assert eng.plan()["groups"][0]["one_warp_rod"]
+
+
+@pytest.mark.parametrize("n", [24, 40])
+def test_one_warp_kernel_extensible(n):
+    # an all-extensible rod (the kernels' GEN form: stretch term, no colour
+    # sweeps), epochs of 50 steps
+    def make():
+        w = World(dt=1e-4, gravity=(0.0, -9.81, 0.0), solver=SolverConfig(iterations=10))
+        w.add_rod(st.init_rod(n + 1, 2e-3 * n, axis=(1.0, 0.0, 0.0)),
+                  st.RodParams(**dict(wl.MATERIAL, stretch_modulus=1e6, extensible=True)))
+        w.finalize()
+        w.clamp_point(0, 0)
+        w.clamp_frame(0, 0)
+        return w
+    parity(make, 200, 50)
+    with Engine(make()) as eng:
+        assert eng.plan()["groups"][0]["one_warp_rod"]
