@@ -146,6 +146,7 @@ struct Group {       // one kernel launch
 // torques carry rounding noise (~1e-300) below the fast path's window, and
 // a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
 constexpr int kSpecMinSteps = 32;
+constexpr int kSpecBackoff = 64;
 bool spec_group(const Group& g) {
     return (g.tier == TIER_STREAM && g.variant == 7) || (g.tier == TIER_CTA && g.variant == 0);
 }
@@ -180,6 +181,17 @@ struct rs_handle_s {
     bool rw1_on = true;             // its one-point-per-lane form (RSB_RW1=0: off)
     int bw_shape = -1;              // its launch shape (RSB_BW_SHAPE, kBwShapes; -1: the planner's)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
+    bool last_spec = false;         // the last launch speculated (rs_last_redo_count)
+    // speculation back-off of one-CTA / one-warp rod groups: a rod whose
+    // dividends keep leaving the fast path's window (rounding noise below
+    // 2^-400) would pay the exact redo launch every epoch.  The redo count
+    // of each speculative launch is copied back asynchronously; three
+    // launches in a row that needed the redo turn speculation off for the
+    // group's next kSpecBackoff launches.
+    std::vector<int> spec_streak, spec_skip;
+    std::vector<cudaEvent_t> redo_ev;
+    std::vector<char> redo_ev_live;
+    int32_t* h_redo = nullptr;      // pinned, one slot per group
     bool dry = false;               // planning only (rs_plan_dry): no CUDA calls
 
     // device mirrors
@@ -1348,8 +1360,38 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // list and returns)
     // (one-CTA rods only for long epochs: the exact launch over the redo
     // list costs a few microseconds, a whole K = 1 step on a short rod)
-    const bool spec = h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
-                      (g.tier != TIER_CTA || steps >= kSpecMinSteps);
+    bool spec = h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
+                (g.tier != TIER_CTA || steps >= kSpecMinSteps);
+    const int gi = int(&g - h->groups.data());
+    const bool backoff = g.tier == TIER_CTA && gi >= 0 && gi < int(h->groups.size());
+    if (spec && backoff) {
+        const size_t ng = h->groups.size();
+        if (h->spec_streak.size() != ng) {
+            h->spec_streak.assign(ng, 0);
+            h->spec_skip.assign(ng, 0);
+            for (cudaEvent_t e : h->redo_ev)
+                if (e) cudaEventDestroy(e);
+            h->redo_ev.assign(ng, nullptr);
+            h->redo_ev_live.assign(ng, 0);
+            if (h->h_redo) cudaFreeHost(h->h_redo);
+            h->h_redo = nullptr;
+            CK(cudaMallocHost(&h->h_redo, sizeof(int32_t) * ng));
+        }
+        // the previous speculative launch's redo count, if it has arrived
+        if (h->redo_ev_live[gi] && cudaEventQuery(h->redo_ev[gi]) == cudaSuccess) {
+            h->redo_ev_live[gi] = 0;
+            h->spec_streak[gi] = h->h_redo[gi] > 0 ? h->spec_streak[gi] + 1 : 0;
+            if (h->spec_streak[gi] >= 3) {
+                h->spec_streak[gi] = 0;
+                h->spec_skip[gi] = kSpecBackoff;
+            }
+        }
+        if (h->spec_skip[gi] > 0) {
+            --h->spec_skip[gi];
+            spec = false;
+        }
+    }
+    h->last_spec = spec;
     if (spec) CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
     auto one = [&](int cfg, int redo_mode) -> cudaError_t {
         auto finish = [&](auto& a) {
@@ -1428,6 +1470,12 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     };
     cudaError_t e = bw ? one_bw() : rw ? one_rw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
     if (e == cudaSuccess && spec) e = one(cfg0, 1);
+    if (e == cudaSuccess && spec && backoff && !h->redo_ev_live[gi]) {
+        if (!h->redo_ev[gi]) CK(cudaEventCreateWithFlags(&h->redo_ev[gi], cudaEventDisableTiming));
+        CK(cudaMemcpyAsync(h->h_redo + gi, h->redo_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaEventRecord(h->redo_ev[gi], h->st));
+        h->redo_ev_live[gi] = 1;
+    }
     if (e != cudaSuccess)
         return fail(RS_E_CUDA, "kernel launch (tier %d variant %d, %d CTAs x %d threads, %zu B smem) failed: %s",
                     g.tier, g.variant, g.ncta, g.threads, g.smem, cudaGetErrorString(e));
@@ -1927,6 +1975,9 @@ void rs_destroy(rs_handle h) {
         if (g.d_halo) cudaFree(g.d_halo);
     }
     for (void* p : h->registered) cudaHostUnregister(p);
+    for (cudaEvent_t e : h->redo_ev)
+        if (e) cudaEventDestroy(e);
+    if (h->h_redo) cudaFreeHost(h->h_redo);
     if (h->d_prof) {   // per-phase profile (RSB_DEBUG=2): cycles per step, CTA 0
         unsigned long long v[PROF_SLOTS];
         if (cudaMemcpy(v, h->d_prof, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess && h->prof_steps > 0) {
@@ -1980,7 +2031,7 @@ int64_t rs_launch_count(rs_handle h) { return h ? h->launches : -1; }
 
 int64_t rs_last_redo_count(rs_handle h) {
     if (!h) return -1;
-    if (!h->redo_count.p) return 0;
+    if (!h->redo_count.p || !h->last_spec) return 0;   // the last launch did not speculate
     if (cudaSetDevice(h->d.device) != cudaSuccess) return -1;
     int32_t n = 0;
     if (cudaMemcpyAsync(&n, h->redo_count.p, sizeof(n), cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||

@@ -605,3 +605,53 @@ def test_one_warp_kernel_extensible(n):
     parity(make, 200, 50)
     with Engine(make()) as eng:
         assert eng.plan()["groups"][0]["one_warp_rod"]
+
+
+def test_speculative_packed_cta_partial_redo_bitwise():
+    # packed one-CTA tasks (variant 0, several rods per CTA) in epochs of
+    # >= 32 steps speculate; CTAs holding a tiny rod are redone by the exact
+    # kernel through the redo list while the others are not -- device epochs
+    # and host epochs (pipelined in chunks: task offsets) both bitwise
+    from paper_2509_04277_b200 import _lib
+    g, r = _tiny_world(40, 9, tiny_every=100), _tiny_world(40, 9, tiny_every=100)
+    with Engine(g) as eng:
+        grp = eng.plan()["groups"][0]
+        assert grp["tier"] == "cta" and grp["variant"] == 0 and not grp["one_warp_rod"]
+        dev = eng.device_world
+        dev.run(40)
+        redone = dev.last_redo_count()
+        dev.download(_lib.RS_STATE)
+        eng.run_epoch(40)   # host arrays in, host arrays out
+    OracleStepper(r).run(80)
+    assert_bitwise(g, r)
+    assert 0 < redone < grp["ctas"], (redone, grp["ctas"])
+
+
+def test_redo_count_reset_without_speculation():
+    # a launch that does not speculate (epoch below 32 steps) reports no
+    # redone rods rather than the previous speculative launch's count
+    g = _tiny_world(1, 16)
+    with Engine(g) as eng:
+        dev = eng.device_world
+        dev.run(40)
+        assert dev.last_redo_count() == 1
+        dev.run(5)
+        assert dev.last_redo_count() == 0
+
+
+def test_speculation_backs_off_for_a_rod_that_always_redoes():
+    # the tiny rod needs the exact kernel at every launch: after three such
+    # launches the group stops speculating (no redo count), and the state
+    # stays bitwise
+    g, r = _tiny_world(1, 16), _tiny_world(1, 16)
+    counts = []
+    with Engine(g) as eng:
+        dev = eng.device_world
+        for _ in range(8):
+            dev.run(40)
+            dev.synchronize()
+            counts.append(dev.last_redo_count())
+        eng.device_world.download(__import__("paper_2509_04277_b200._lib", fromlist=["RS_STATE"]).RS_STATE)
+    OracleStepper(r).run(320)
+    assert_bitwise(g, r)
+    assert counts[:3] == [1, 1, 1] and 0 in counts[3:], counts
