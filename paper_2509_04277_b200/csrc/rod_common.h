@@ -154,10 +154,12 @@ struct StepArgs {
     Real *cnorm, *cdepth, *cacc_n, *cacc_t;        // (P,3) (P) (P) (P)
     unsigned long long *contacts;                  // active contacts after the last step
     Real coll_margin, restitution, mu;
-    // self-collision (_core.pyx:665-708, 956-980): CTA tier, thread 0
+    // self-collision (_core.pyx:665-708, 956-980): CTA tier; broad phase by
+    // the whole CTA (list order kept by a prefix sum), pair impulses thread 0
     int32_t has_self, n_groups, excl, pair_cap;
     const int32_t *grp_rod, *grp_gi, *grp_s, *grp_e;
     Real* grp_c;                                   // (G,3) scratch
+    int32_t* gp_count;                             // (G(G-1)/2) scratch: pairs per group pair
     int32_t *pair_a, *pair_b, *pair_count;         // pair list, CNT_PAIRS (persistent)
     Real *pair_md, *pair_acc;
     Real touch, broad;

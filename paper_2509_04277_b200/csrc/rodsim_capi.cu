@@ -202,7 +202,7 @@ struct rs_handle_s {
     DevBuf nmin, nmax, verts, nstart, ncount, torder, tris, cradii, cmask;
     DevBuf cact, cnorm, cdepth, cacc_n, cacc_t;
     // self-collision: group table (static), pair list (state), count (device)
-    DevBuf grp_rod, grp_gi, grp_s, grp_e, grp_c, pair_a, pair_b, pair_md, pair_acc;
+    DevBuf grp_rod, grp_gi, grp_s, grp_e, grp_c, gp_count, pair_a, pair_b, pair_md, pair_acc;
     int32_t* d_pairs = nullptr;             // CNT_PAIRS, persistent like the ctx counter
     int contacts_on = 0;                    // any contact machinery needed
     unsigned long long* d_contacts = nullptr;
@@ -527,7 +527,10 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
             }
 
     // -- choose tiers --------------------------------------------------------
-    const int cta_cap = d.force_tier == TIER_CTA ? kVariants[kNumCapVariants - 1].cover() : kCtaMaxPoints;
+    // (self-colliding scenes: any one CTA -- the pair list couples arbitrary
+    // points -- up to the largest variant)
+    const int cta_cap = (d.force_tier == TIER_CTA || d.has_self) ? kVariants[kNumCapVariants - 1].cover() + 1
+                                                                 : kCtaMaxPoints;
     const int clu_cap = kVariants[kNumCapVariants - 1].cover();
     std::vector<int> seg_tier(segs.size());
     int64_t max_cta_seg = 0;
@@ -589,6 +592,9 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     if (max_cta_seg > 0) {
         int v = 0;
         while (kVariants[v].cover() + 1 < max_cta_seg) ++v;
+        // the scene-feature kernels (contacts, self-collision, live) carry
+        // the CTA variants 0-2 and 4
+        if (v == 3 && (h->contacts_on || d.has_self || d.live)) v = 4;
         // batches of short rods: one rod per 64-thread CTA, 5 CTAs per SM
         int64_t cta_points = 0;
         for (size_t i = 0; i < segs.size(); ++i)
@@ -1112,6 +1118,9 @@ int upload_static(rs_handle h) {
         if ((rc = put_i32(h, h->grp_s, d.grp_s, size_t(d.n_groups)))) return rc;
         if ((rc = put_i32(h, h->grp_e, d.grp_e, size_t(d.n_groups)))) return rc;
         if ((rc = dev_alloc(h->grp_c, h->rsz * 3 * size_t(d.n_groups)))) return rc;
+        const size_t ngp = size_t(d.n_groups) * size_t(d.n_groups - 1) / 2;
+        // (per-thread pair counts of the broad phase's scan: one CTA)
+        if ((rc = dev_alloc(h->gp_count, sizeof(int32_t) * std::max<size_t>(ngp, 1024)))) return rc;
     }
 
     if ((rc = put_real(h, h->cradii, d.cradii, P))) return rc;
@@ -1313,6 +1322,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.grp_s = static_cast<const int32_t*>(h->grp_s.p);
     a.grp_e = static_cast<const int32_t*>(h->grp_e.p);
     a.grp_c = static_cast<Real*>(h->grp_c.p);
+    a.gp_count = static_cast<int32_t*>(h->gp_count.p);
     a.pair_a = static_cast<int32_t*>(h->pair_a.p);
     a.pair_b = static_cast<int32_t*>(h->pair_b.p);
     a.pair_md = static_cast<Real*>(h->pair_md.p);
@@ -1967,7 +1977,7 @@ void rs_destroy(rs_handle h) {
                       &h->pt_elem, &h->tasks, &h->binds, &h->drvs, &h->grabs, &h->nmin, &h->nmax, &h->verts,
                       &h->nstart, &h->ncount, &h->torder, &h->tris, &h->cradii, &h->cmask, &h->cact, &h->cnorm,
                       &h->cdepth, &h->cacc_n, &h->cacc_t, &h->grp_rod, &h->grp_gi, &h->grp_s, &h->grp_e,
-                      &h->grp_c, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc, &h->g_act_d, &h->g_pt_d,
+                      &h->grp_c, &h->gp_count, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc, &h->g_act_d, &h->g_pt_d,
                       &h->g_tgt_d, &h->redo_list, &h->redo_count})
         if (b->p) cudaFree(b->p);
     for (Group& g : h->groups) {

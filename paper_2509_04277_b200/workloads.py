@@ -174,16 +174,17 @@ def knot():
     return w
 
 
-def crossing(points=24, interval=1):
+def crossing(points=24, interval=1, length=0.05):
     """Two rods crossing 1.5 mm apart and pushed together: self-collision
-    pairs between rods (quick fixture for the pair phase)."""
+    pairs between rods (quick fixture for the pair phase; points=257,
+    length=0.5 is the paper's 2 x 256-element size)."""
     from .selfcollide import SelfCollisionConfig
     w = World(dt=1e-4, gravity=(0.0, 0.0, 0.0), solver=SolverConfig(iterations=10),
               self_collision=SelfCollisionConfig(group_size=4, sphere_radius=0.01,
                                                  neighbor_exclusion=2, point_radius=1e-3))
-    w.add_rod(st.init_rod(points, 0.05, axis=(1.0, 0.0, 0.0), origin=(-0.025, 0.0, 0.0)),
+    w.add_rod(st.init_rod(points, length, axis=(1.0, 0.0, 0.0), origin=(-length / 2, 0.0, 0.0)),
               st.RodParams(**THREAD))
-    w.add_rod(st.init_rod(points, 0.05, axis=(0.0, 1.0, 0.0), origin=(0.0, -0.025, 0.0015)),
+    w.add_rod(st.init_rod(points, length, axis=(0.0, 1.0, 0.0), origin=(0.0, -length / 2, 0.0015)),
               st.RodParams(**THREAD))
     w.finalize()
     w.collision_interval = interval

@@ -154,8 +154,12 @@ def test_self_collision_plan_is_one_cta():
     assert len(g) == 1 and g[0]["tier"] == "cta" and g[0]["ctas"] == 1 and g[0]["points"] == 96
     from paper_2509_04277_b200.constraints import SolverConfig
     from paper_2509_04277_b200.selfcollide import SelfCollisionConfig
+    # the paper's knot size (2 x 257 points) and up to the largest one-CTA
+    # variant (1153 points) plan into one CTA; beyond that, rejected
+    big = plan(wl.crossing(points=257, length=0.512))
+    assert len(big) == 1 and big[0]["tier"] == "cta" and big[0]["points"] == 514 and big[0]["variant"] == 4
     w = World(dt=1e-4, solver=SolverConfig(), self_collision=SelfCollisionConfig())
-    for _ in range(3):
+    for _ in range(5):
         w.add_rod(st.init_rod(300, 0.3), st.RodParams())
     w.finalize()
     with pytest.raises(NotImplementedError, match="self-collision"):

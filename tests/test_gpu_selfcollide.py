@@ -37,6 +37,27 @@ def test_crossing_bitwise(interval, k):
         assert np.array_equal(_bits(getattr(g, key)), _bits(getattr(r, key))), key
 
 
+@pytest.mark.parametrize("points", [257, 400])
+def test_self_collision_beyond_513_points_bitwise(points):
+    # the paper's knot size, 2 x 256 elements = 514 points, and larger: one
+    # CTA of the largest variant, the broad phase built by the whole CTA
+    # (ordered scan), the pair impulses in list order
+    g, r = wl.crossing(points=points, length=0.002 * (points - 1)), \
+        wl.crossing(points=points, length=0.002 * (points - 1))
+    ref = OracleStepper(r)
+    counts = []
+    with Engine(g) as eng:
+        grp = eng.plan()["groups"][0]
+        assert grp["tier"] == "cta" and grp["points"] == 2 * points and grp["self_collision"]
+        for _ in range(12):
+            counts.append(eng.run_epoch(10)["contacts"])
+            ref.run(10)
+            assert counts[-1] == ref.contacts
+    assert max(counts) > 0
+    for key in STATE:
+        assert np.array_equal(_bits(getattr(g, key)), _bits(getattr(r, key))), key
+
+
 def test_knot_replay_bitwise():
     sched = load_replay(os.path.join(GOLDEN, "knot_session.ndjson"))
     g, r = wl.knot(), wl.knot()
