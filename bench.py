@@ -333,6 +333,21 @@ def latency_floor(plan, us, k, lat, iters=10, ext=False, t_launch_us=0.0):
     (PHASE_CHAIN; halo loads of a multi-CTA tier are DSMEM reads)."""
     n_sync = plan["sync_per_step"]
     t_sync = barrier_ns(plan)
+    halo = plan.get("halo")
+    if halo:
+        # wide-halo kernel (rod_halo.cuh): every phase ends at a CTA barrier
+        # of halo["threads"], the step at one inter-CTA exchange (cluster
+        # barrier, or the grid's neighbour flags)
+        from paper_2509_04277_b200 import _lib
+        sweeps = plan["any_dist"] or plan["bindings"]
+        n_sync = 1 + ((1 + iters * (2 + (1 if plan["bindings"] else 0))) if sweeps else 0) + \
+            (1 if halo["exchange"] == "grid" else 0)
+        t_sync = _lib.micro("bar_sync", halo["threads"])[1]
+        if halo["ctas"] > 1:
+            t_x = (_lib.micro("grid_flags", halo["ctas"])[1] if halo["exchange"] == "grid"
+                   else _lib.micro("cluster_barrier", halo["ctas"])[1])
+        else:
+            t_x = t_sync
 
     def cyc(ph, extra_d=0):
         # (a multi-CTA tier's halo loads are DSMEM reads; its measured t_sync
@@ -352,10 +367,17 @@ def latency_floor(plan, us, k, lat, iters=10, ext=False, t_launch_us=0.0):
     chain += iters * per_it
     t_chain_us = chain / lat["ghz"] / 1e3
     t_sync_us = n_sync * t_sync / 1e3
+    out = {"n_sync": n_sync, "t_sync_ns": t_sync}
+    if halo:
+        t_sync_us += t_x / 1e3
+        out.update({"n_exchange": 1, "t_exchange_ns": t_x, "exchange": halo["exchange"],
+                    "model": "n_sync t_bar(CTA) + t_exchange + t_chain + t_launch/K"})
+    else:
+        out["model"] = "n_sync t_sync + t_chain + t_launch/K"
     floor = t_sync_us + t_chain_us + t_launch_us / k
-    return {"n_sync": n_sync, "t_sync_ns": t_sync, "sync_us": t_sync_us, "t_chain_us": t_chain_us,
-            "chain_cycles": chain, "t_launch_us": t_launch_us, "k": k, "t_floor_us": floor,
-            "frac": floor / us, "model": "n_sync t_sync + t_chain + t_launch/K"}
+    out.update({"sync_us": t_sync_us, "t_chain_us": t_chain_us, "chain_cycles": chain,
+                "t_launch_us": t_launch_us, "k": k, "t_floor_us": floor, "frac": floor / us})
+    return out
 
 
 def single_rod_suite(precision):
@@ -386,7 +408,7 @@ def single_rod_suite(precision):
 
     def row(name, make, k, launches, cpu_name, cpu_args=(), cpu_steps=200, ext=False, **extra):
         us, plan = device_us(make, k, launches)
-        r = {"us_per_step": us, "k": k, "tier": plan["tier"], "ctas": plan["ctas"],
+        r = {"us_per_step": us, "k": k, "tier": plan["tier"], "ctas": plan["ctas"], "halo": plan.get("halo"),
              "roofline": latency_floor(plan, us, k, lat, ext=ext, t_launch_us=t_launch)}
         r.update(br.single_rod_cpu(cpu_name, cpu_args, steps=cpu_steps))
         r["speedup_vs_cpu"] = r["cpu_us_per_step"] / us
@@ -427,6 +449,7 @@ def single_rod_suite(precision):
             r[f"k{k}"] = us
         r["tier"] = plan["tier"]
         r["ctas"] = plan["ctas"]
+        r["halo"] = plan.get("halo")
         r["roofline_k100"] = latency_floor(plan, r["k100"], 100, lat, t_launch_us=t_launch)
         r["roofline_k1"] = latency_floor(plan, r["k1"], 1, lat, t_launch_us=t_launch)
         c = br.single_rod_cpu("sweep", (n,), steps=max(3, 20000 // n), par_steps=max(3, 5000 // n))

@@ -110,7 +110,7 @@ SIGNATURES = [
 
 MICRO_KINDS = {"dadd": 0, "dmul": 1, "dfma": 2, "div": 3, "sqrt_add": 4, "div_rn": 5,
                "rcp": 6, "lds": 7, "bar_sync": 8, "cluster_barrier": 9, "dsmem": 10,
-               "neighbour_sync": 11}
+               "neighbour_sync": 11, "grid_flags": 12}
 
 
 def micro(kind, param=0):

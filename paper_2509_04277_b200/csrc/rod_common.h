@@ -47,6 +47,13 @@ struct CtaTask {
     int32_t nrods;       // whole rods in the range (0: part of one rod)
 };
 
+// Wide-halo cluster kernel (rod_halo.cuh): one CTA's local point-index
+// ranges along the rod(s) of the launch -- owned [o0, o1), held [x0, x1)
+// (owned plus up to G ghost points per side)
+struct HaloTask {
+    int32_t o0, o1, x0, x1;
+};
+
 // A binding endpoint pair resolved to (cta rank within the cluster, slot).
 struct BindEntry {
     int32_t a_rank, a_slot;
@@ -177,6 +184,15 @@ struct StepArgs {
     // _core.pyx:453-471): scene-feature kernels only; thread 0 of every CTA
     // adds the SM cycles it spent inside barriers (null: off)
     unsigned long long* bar_cycles;
+    // wide-halo cluster kernel: per-CTA ranges, per-point driver rods
+    // (2 per point: point driver, frame driver; -1 none), per-point binding
+    // code (-1 none; bit 0: endpoint a, bit 1: bidirectional), the launch's
+    // rods (NR <= 2, np points each, first point / element), thread stride
+    // per rod W and ghost width G
+    const HaloTask* htask;
+    const int32_t *hdrv, *hbind;
+    int32_t h_nr, h_np, h_w, h_g;
+    int32_t h_poff[2], h_eoff[2];
 };
 
 constexpr int PROF_SLOTS = 64;

@@ -1,0 +1,704 @@
+// rod_halo.cuh -- wide-halo cluster kernel: a rod (or a pair of rods bound
+// point to point) spread over the CTAs of a thread-block cluster with ONE
+// cluster barrier per time step.
+//
+// The general cluster tier (rod_step.cuh) issues a cluster barrier after each
+// of the 2I+3 (3I+3 with bindings) phases of a step, ~300 ns each: 33 x 300 ns
+// is ~10 us of the cfg3 pair's 22 us step.  Here every CTA owns a contiguous
+// range [o0, o1) of local point indices and also keeps G = 2I+1 ghost points
+// on either side, whose state it receives from its neighbours once per step.
+// A step's dependency radius along a rod is scatter 1 (element i reads point
+// i+1) + gather 1 (point i reads element i-1) + one per colour phase (2I);
+// bindings couple the same local index of the two rods (radius 0, both rods'
+// columns live in the same CTA).  Computing the whole step redundantly on
+// [o0-G, o1+G) therefore leaves the owned range exact, and the only
+// inter-CTA exchange is the owned boundary state (pos, vel, q, w of G points
+// per side) pushed into the neighbours' ghost slots through distributed
+// shared memory before the step's one cluster barrier.  Every other phase
+// boundary is a CTA barrier (bar.sync, 15-50 ns).
+//
+// Layout: thread t = r W + j holds point i = x0 + j of rod r (r < NR <= 2;
+// W = the widest extended range of the launch) and the element i -- one point
+// per thread, its state in registers, neighbours through shared memory.  The
+// colour phases use the one-warp kernel's formulation (rod_warp1.cuh): both
+// endpoints of an element compute its impulse from the same inputs with the
+// same operations (the upper end holding the tangent negated), so each
+// thread moves only its own point and a phase is one shared-memory round trip
+// through a ping-pong velocity buffer.  Bindings are done the same way by
+// the two threads of a bound column.
+//
+// Shared memory: the per-thread state fields are double-buffered by step
+// parity -- the owned boundary points of step s are pushed into the
+// neighbours' buffer (s+1)&1 while a slower neighbour may still read buffer
+// s&1 of step s (the cluster barrier of step s orders the reuse).
+//
+// Quotients outside the fast path's window take the IEEE division inline
+// (one warp-uniform test per group of quotients); dividends below 2^-400 --
+// the rounding noise a planar rod carries in its out-of-plane components --
+// are first scaled by 2^700 for the correctly rounded reciprocal-based
+// quotient and scaled back (exact while the quotient is a normal number), so
+// only quotients that come out subnormal take that branch.  What remains
+// speculative -- degenerate segments, non-finite forces (both stamp the
+// reference's error step), colour-phase and binding dividends outside the
+// window -- is ANDed into a per-thread flag, for the results the owned range
+// depends on (a ghost's result of a phase matters while its distance outside
+// the owned range is within the radius still to come; the outer ghost shell
+// computes garbage from missing neighbours).  At the end of the launch the
+// cluster votes; if anything failed, nothing is written back and the flag in
+// A.redo_count makes the exact general cluster kernel, launched right after
+// in consume mode, step the segment again from the launch-start state (it
+// exits at once otherwise).
+//
+// Arithmetic: the reference's expression order (oracle/rod_oracle.c cites
+// _core.pyx), identical to rod_warp1.cuh / rod_step.cuh.
+#pragma once
+
+#include "rod_warp1.cuh"
+
+namespace rsb {
+
+// the state fields (double-buffered) and the per-step fields, T Reals each
+enum HaloField : int {
+    HL_P = 0, HL_V = 3, HL_Q = 6, HL_W = 10, HL_NSTATE = 13,   // x 2 (parity)
+    HL_EF = 26, HL_FN = 29, HL_JT = 33, HL_NN = 36, HL_B = 39,  // scatter outputs
+    HL_VA = 40, HL_VB = 43,                                      // colour ping-pong
+    HL_NF = 46,
+};
+__host__ __device__ constexpr size_t halo_smem_bytes(int threads, size_t rsz) {
+    return align16(size_t(HL_NF) * size_t(threads) * rsz) + 16;
+}
+
+// a / b for a dividend of any magnitude whose quotient is a normal number
+// (fp64 mirror mode): dividends below the window are scaled by 2^600 (exact),
+// divided with the correctly rounded reciprocal-based quotient, and scaled
+// back (exact for a normal quotient, so the bits are IEEE a / b's).  The
+// scaling factors are 1 for every other dividend, so the instruction stream
+// is the same for all.  The operand checks are ANDed into ok.
+template <typename R>
+__device__ __forceinline__ R hl_quot(R a, R b, R rb, bool& ok) {
+#if defined(RSB_MODE_ID) && RSB_MODE_ID == 0
+    if constexpr (sizeof(R) == 8) {
+        const unsigned ha = unsigned(__double2hiint(a)) & 0x7fffffffu;
+        const bool tiny = ha < ((1023u - 400u) << 20);   // [0, 2^-400): x 2^700 -> [0, 2^300)
+        const R s = tiny ? R(0x1p700) : R(1.0);
+        const R si = tiny ? R(0x1p-700) : R(1.0);
+        const R as = a * s;
+        const R q = bw_quot(as, b, rb) * si;
+        const unsigned eq = unsigned(__double2hiint(q)) & 0x7ff00000u;
+        ok = ok & dividend_ok(as) & (!tiny | is_zero(a) | (eq != 0u));
+        return q;
+    }
+#endif
+    ok = ok & dividend_ok(a);
+    return bw_quot(a, b, rb);
+}
+// N quotients by one divisor (window b_ok checked by the caller), exact: a
+// lane whose operands leave the fast path's range and whose result matters
+// (need) takes the IEEE division, behind one warp-uniform test -- dividends
+// whose quotient is subnormal (decaying out-of-plane noise) reach it.
+template <int N, typename R>
+__device__ __forceinline__ void hl_div(const R (&a)[N], R b, R rb, bool b_ok, bool need, R (&q)[N]) {
+    bool qok = b_ok;
+#pragma unroll
+    for (int k = 0; k < N; ++k) q[k] = hl_quot(a[k], b, rb, qok);
+    const bool slow = need & !qok;
+    if (__any_sync(0xffffffffu, slow)) {
+        if (slow)
+#pragma unroll
+            for (int k = 0; k < N; ++k) q[k] = div_ieee(a[k], b);
+    }
+}
+
+// TB: the launch's thread bound (registers: 256 -> up to 255, 512 -> 128).
+// GX: a co-resident grid instead of one cluster (rods longer than 16 CTAs
+// hold, or spread thinner): the owned boundary state goes through a
+// double-buffered global halo record per CTA and side, published with a
+// release flag per CTA that the two neighbours acquire -- still one exchange
+// per step.
+template <typename Real, int MODE, bool GEN, bool BIND, int TB, bool GX>
+__global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* sm = reinterpret_cast<Real*>(smem_raw);
+    const int T = blockDim.x, t = threadIdx.x;
+    const unsigned rank = GX ? blockIdx.x : cluster_rank();
+    const unsigned ncl = gridDim.x;   // one cluster (or one co-resident grid) per launch
+    const HaloTask tk = A.htask[rank];
+    const int NR = A.h_nr, W = A.h_w, np = A.h_np, ne = np - 1;
+    const int r = t / W, j = t - r * W;
+    const int i = tk.x0 + j;                        // local index along the rod
+    const bool pv = r < NR && i < tk.x1;            // thread holds a point
+    const bool ev = pv && i < ne;                   // ... and its element
+    const bool own = pv && i >= tk.o0 && i < tk.o1;
+    const int rr = pv ? r : 0;
+    const int pt = A.h_poff[rr] + (pv ? i : 0);
+    const int el = A.h_eoff[rr] + (ev ? i : 0);
+#define HS(f, x) sm[(f) * T + (x)]
+    const Real dt = A.dt, beta = A.beta;
+    const Real rdt = Real(1.0) / dt;
+    const bool dt_ok = in_window(dt);
+    const Real grav[3] = {A.gx, A.gy, A.gz};
+    const bool l_ok = in_window(A.u.l);
+    const bool I_ok = in_window(A.u.I[0]) & in_window(A.u.I[1]) & in_window(A.u.I[2]);
+    bool ok = true;
+    // Which results the owned range depends on: a thread's result of a
+    // phase matters while its distance outside [o0, o1) is within the
+    // dependency radius still to come (the outer ghost shell computes garbage
+    // from missing neighbours and must neither fail the vote nor take the
+    // IEEE fallback).  Rg: radius after the gather (2I with colour sweeps).
+    const int d_l = tk.o0 - i, d_r = i - (tk.o1 - 1);
+    const int dout = max(max(d_l, d_r), 0);
+    const int Rg = A.h_g - 1;
+    const bool m_sc = pv && d_l <= Rg + 1 && d_r <= Rg;   // scatter of element i
+    const bool m_ga = pv && dout <= Rg;                   // gather of point / frame i
+
+    // neighbours' thread index of a pushed point (same W everywhere)
+    const bool has_l = rank > 0, has_r = rank + 1 < ncl;
+    const int x0_l = has_l ? A.htask[rank - 1].x0 : 0;
+    const int x0_r = has_r ? A.htask[rank + 1].x0 : 0;
+    const int G = A.h_g;
+    const bool push_l = own && has_l && i < tk.o0 + G;
+    const bool push_r = own && has_r && i >= tk.o1 - G;
+    Real* sm_l = sm;
+    Real* sm_r = sm;
+    if constexpr (!GX) {
+        if (has_l) sm_l = cg::this_cluster().map_shared_rank(sm, rank - 1);
+        if (has_r) sm_r = cg::this_cluster().map_shared_rank(sm, rank + 1);
+    }
+    // grid exchange: one side's record = NR x G points x 13 state words
+    const size_t hrec = size_t(NR) * size_t(G) * HL_NSTATE;
+    const int t_l = r * W + (i - x0_l), t_r = r * W + (i - x0_r);
+
+    // ---- state and statics ----
+    Real p[3], v[3], q[4], w[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        p[k] = A.pos[3 * size_t(pt) + k];
+        v[k] = A.vel[3 * size_t(pt) + k];
+        w[k] = A.w[3 * size_t(el) + k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = A.q[4 * size_t(el) + k];
+    const uint32_t fl = A.pflags[pt];
+    const bool pl = (fl & SF_PLOCK) != 0, flk = (fl & SF_FLOCK) != 0;
+    const bool dist = (fl & SF_DIST) != 0, ext = (fl & SF_EXT) != 0;
+    const Real m = A.mass[pt], rm = rcp_rn(m), im = A.invm[pt];
+    const bool m_ok = in_window(m);
+    // element i: w_sum = im_i + im_{i+1}; element i-1: im_{i-1} + im_i (the
+    // same operands in the same order as the thread that owns it)
+    const Real im_up = ev ? A.invm[pt + 1] : Real(0);
+    const Real ws = im + im_up;
+    const Real rws = rcp_rn(ws);
+    const bool act = ev && dist && !(ws <= Real(0));
+    ok = ok & !(m_ga & act & !in_window(ws));
+    const bool hl = pv && i > 0;   // element i-1 exists
+    const uint32_t fl_l = hl ? A.pflags[pt - 1] : 0u;
+    const Real ws_l = (hl ? A.invm[pt - 1] : Real(0)) + im;
+    const Real rws_l = rcp_rn(ws_l);
+    const bool act_l = hl && (fl_l & SF_DIST) && !(ws_l <= Real(0));
+    ok = ok & !(m_ga & act_l & !in_window(ws_l));
+    // colour c: the element of colour c containing point i -- its own
+    // (lower end) when i % 2 == c, the left one (upper end) otherwise
+    const bool a_side[2] = {(i & 1) == 0, (i & 1) == 1};
+    const int partner[2] = {(i & 1) ? t - 1 : t + 1, (i & 1) ? t + 1 : t - 1};
+    Real wsP[2], rwsP[2];
+    bool actP[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        wsP[c] = a_side[c] ? ws : ws_l;
+        rwsP[c] = a_side[c] ? rws : rws_l;
+        actP[c] = (a_side[c] ? act : act_l) && pv;
+    }
+    // drivers (_core.pyx:866-875): the rod driving this point / this frame
+    const int drp = pv ? A.hdrv[2 * pt] : -1, drf = ev ? A.hdrv[2 * pt + 1] : -1;
+    Real dvel[3] = {Real(0), Real(0), Real(0)}, drot = Real(0);
+    if (drp >= 0)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dvel[k] = A.drv_v[3 * drp + k];
+    if (drf >= 0) drot = A.drv_rot[drf];
+    // bindings: the point at the same local index of the other rod
+    const int hb = (BIND && pv) ? A.hbind[pt] : -1;
+    const bool bnd = hb >= 0;
+    const bool b_is_a = (hb & 1) != 0;
+    const int t_b = (1 - rr) * W + j;
+    Real bw_own = Real(0), bws = Real(0), brws = Real(0);
+    if constexpr (BIND) {
+        const Real im_o = bnd ? A.invm[A.h_poff[1 - rr] + i] : Real(0);
+        const bool bi = (hb & 2) != 0;
+        const Real wa = bi ? (b_is_a ? im : im_o) : Real(0);
+        const Real wb = b_is_a ? im_o : im;
+        bws = wa + wb;
+        brws = rcp_rn(bws);
+        bw_own = b_is_a ? wa : wb;
+    }
+    const bool b_upd = bnd && (!b_is_a || bw_own > Real(0));   // one-way: a is never moved
+
+    int cur = 0;   // state buffer of this step
+    for (int step = 0; step < A.steps; ++step) {
+        const int sb = cur * HL_NSTATE;
+        if (!GX && step > 0 && !own) {   // ghosts: the state the neighbours pushed
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                p[k] = HS(sb + HL_P + k, t);
+                v[k] = HS(sb + HL_V + k, t);
+                w[k] = HS(sb + HL_W + k, t);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = HS(sb + HL_Q + k, t);
+        }
+        if (step == 0 || GX) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                HS(sb + HL_P + k, t) = p[k];
+                HS(sb + HL_V + k, t) = v[k];
+                HS(sb + HL_W + k, t) = w[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) HS(sb + HL_Q + k, t) = q[k];
+            __syncthreads();
+        }
+
+        // ============ scatter (_core.pyx:745-805): element i ============
+        Real pb[3], vb[3], qb[4], wb[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            pb[k] = HS(sb + HL_P + k, t + 1);
+            vb[k] = HS(sb + HL_V + k, t + 1);
+            wb[k] = HS(sb + HL_W + k, t + 1);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) qb[k] = HS(sb + HL_Q + k, t + 1);
+        Real d[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d[k] = pb[k] - p[k];
+        const Real dd = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+        const bool sc = m_sc & ev;
+        const bool dd_ok = in_window(dd);
+        ok = ok & (!sc | dd_ok);   // a degenerate segment: the exact kernel stamps it
+        const Real len = sqrt_rn(dd);
+        const Real rlen = rcp_rn(len);
+        // the phase's quotients on the fast path; a lane that needs one
+        // outside its range recomputes them all with IEEE divisions, behind
+        // one warp-uniform test for the phase
+        bool slow = false;
+        auto fq = [&](Real a, Real b, Real rb, bool b_ok, bool need) -> Real {
+            bool qok = b_ok;
+            const Real x = hl_quot(a, b, rb, qok);
+            slow = slow | (need & !qok);
+            return x;
+        };
+        const Real bnum = beta * (len - A.u.l);
+        Real bias = fq(bnum, dt, rdt, dt_ok, sc & dist);
+        Real t3[3], nn[3], pair[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t3[k] = fq(d[k], len, rlen, dd_ok, sc);
+        Real kpl_len = fq(A.u.kpl, len, rlen, dd_ok, sc);
+        Real v3 = Real(0);
+        if constexpr (GEN) v3 = fq(len, A.u.l, A.u.il, l_ok, sc & ext);
+        // binding constants of this step (start-of-step positions,
+        // _core.pyx:981-1001): d = p_b - p_a on both threads of the column
+        Real bd[3] = {Real(0), Real(0), Real(0)}, bnq[3] = {Real(0), Real(0), Real(0)};
+        Real bdist = Real(0), bbias = Real(0);
+        bool bact = false;
+        if constexpr (BIND) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const Real po = HS(sb + HL_P + k, t_b);
+                bd[k] = b_is_a ? po - p[k] : p[k] - po;
+            }
+            const Real bdd = bd[0] * bd[0] + bd[1] * bd[1] + bd[2] * bd[2];
+            bact = bnd && !(bdd == Real(0)) && !(bws == Real(0));
+            const bool bneed = bact && dout <= Rg - 2;   // the first binding phase's cone
+            bdist = sqrt_rn(bdd);
+            const Real rbd = rcp_rn(bdist);
+            const bool bdd_ok = in_window(bdd);
+            ok = ok & (!bneed | (bdd_ok & in_window(bws)));
+#pragma unroll
+            for (int k = 0; k < 3; ++k) bnq[k] = fq(bd[k], bdist, rbd, bdd_ok, bneed);
+            bbias = fq(beta * bdist, dt, rdt, dt_ok, bneed);
+        }
+        if (__any_sync(0xffffffffu, slow)) {
+            if (slow) {
+                bias = div_ieee(bnum, dt);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) t3[k] = div_ieee(d[k], len);
+                kpl_len = div_ieee(A.u.kpl, len);
+                if constexpr (GEN) v3 = div_ieee(len, A.u.l);
+                if constexpr (BIND) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) bnq[k] = div_ieee(bd[k], bdist);
+                    bbias = div_ieee(beta * bdist, dt);
+                }
+            }
+        }
+        Real bn[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            pair[k] = Real(0);
+            nn[k] = t3[k];
+            bn[k] = b_is_a ? bnq[k] : -bnq[k];
+        }
+        if constexpr (GEN) {   // stretch, Eq. 2
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const Real g = pair[k] - A.u.ks * (v3 - Real(1.0)) * t3[k];
+                pair[k] = ext ? g : pair[k];
+            }
+        }
+        Real d3v[3], er[3], f4[4], fo[4], fn[4], ef[3], jt[3];
+        dir3(q, d3v);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) er[k] = t3[k] - d3v[k];
+        Real dotp = er[0] * t3[0] + er[1] * t3[1] + er[2] * t3[2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) pair[k] = pair[k] - kpl_len * (er[k] - dotp * t3[k]);
+        dir3_jt(q, er, f4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fo[k] = A.u.kpl * f4[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ef[k] = -pair[k] + A.u.gt * (vb[k] - v[k]);
+        const bool jv = i + 1 < ne;   // junction i|i+1 inside the rod
+        {
+            dotp = q[0] * qb[0] + q[1] * qb[1] + q[2] * qb[2] + q[3] * qb[3];
+            const Real sgn = dotp < Real(0) ? Real(-1.0) : Real(1.0);
+            const Real il = A.u.il;
+            Real qnn[4], qp[4], u[3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                qnn[k] = sgn * qb[k];
+                qp[k] = (qnn[k] - q[k]) * il;
+            }
+            conj_prod_vec(q, qp, u);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) u[k] = u[k] * Real(2.0);
+            const Real two_il = Real(2.0) * il;
+            const Real mtwo_il = Real(-2.0) * il;
+            Real fob[4], fnb[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                fob[k] = fo[k];
+                fnb[k] = Real(0);
+            }
+            auto bend = [&](auto kc) {
+                constexpr int K = decltype(kc)::value;
+                const Real du = u[K] - A.u.us[K];
+                const Real coeff = A.u.kb[K] * du * A.u.l;
+                Real bp[4], ba[4];
+                bform<K>(qp, bp);
+                bform<K>(q, ba);
+                const Real sc = sgn * coeff;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const Real ga = Real(2.0) * bp[x] + two_il * ba[x];
+                    const Real gn = mtwo_il * ba[x];
+                    fob[x] = fob[x] - coeff * ga;
+                    fnb[x] = fnb[x] - sc * gn;
+                }
+            };
+            bend(std::integral_constant<int, 0>{});
+            bend(std::integral_constant<int, 1>{});
+            bend(std::integral_constant<int, 2>{});
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                fo[k] = jv ? fob[k] : fo[k];
+                fn[k] = jv ? fnb[k] : Real(0);
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const Real j3 = A.u.gr * (wb[k] - w[k]);
+                jt[k] = jv ? j3 : Real(0);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            HS(HL_EF + k, t) = ef[k];
+            HS(HL_JT + k, t) = jt[k];
+            HS(HL_NN + k, t) = nn[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) HS(HL_FN + k, t) = fn[k];
+        HS(HL_B, t) = bias;
+        __syncthreads();
+
+        // ============ gather (_core.pyx:808-875): point i, frame i ============
+        Real efl[3], fnl[4], jtl[3], nn_l[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            efl[k] = HS(HL_EF + k, t - 1);
+            jtl[k] = HS(HL_JT + k, t - 1);
+            nn_l[k] = HS(HL_NN + k, t - 1);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fnl[k] = HS(HL_FN + k, t - 1);
+        const Real bias_l = HS(HL_B, t - 1);
+        Real a_v[3], dvv[3], a_w[3], dww[3];
+        slow = false;
+        {
+            const bool hp = i > 0;
+            Real f[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                f[k] = m * grav[k];
+                f[k] = f[k] + ((GEN && A.has_fext) ? A.fext[3 * size_t(pt) + k] : Real(0));
+                const Real g0 = f[k] + ef[k];   // the point's own element (not the last point)
+                f[k] = ev ? g0 : f[k];
+                const Real g = f[k] - efl[k];
+                f[k] = hp ? g : f[k];
+            }
+            ok = ok & (!m_ga | (isfinite(f[0]) & isfinite(f[1]) & isfinite(f[2])));
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a_v[k] = dt * f[k];
+                dvv[k] = fq(a_v[k], m, rm, m_ok, m_ga & !pl);
+            }
+        }
+        {   // frame i
+            const bool jp = i > 0;
+            Real F[4], tau[3], iw[3], gy[3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const Real g = fo[k] + fnl[k];
+                F[k] = jp ? g : fo[k];
+            }
+            const Real dot = F[0] * q[0] + F[1] * q[1] + F[2] * q[2] + F[3] * q[3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) F[k] = F[k] - dot * q[k];
+            conj_prod_vec(q, F, tau);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                tau[k] = tau[k] * Real(0.5);
+                const Real g = tau[k] + jt[k];
+                tau[k] = jv ? g : tau[k];
+                const Real g2 = tau[k] - jtl[k];
+                tau[k] = jp ? g2 : tau[k];
+            }
+            ok = ok & (!(m_ga & ev) | (isfinite(tau[0]) & isfinite(tau[1]) & isfinite(tau[2])));
+#pragma unroll
+            for (int k = 0; k < 3; ++k) iw[k] = A.u.I[k] * w[k];
+            gy[0] = w[1] * iw[2] - w[2] * iw[1];
+            gy[1] = w[2] * iw[0] - w[0] * iw[2];
+            gy[2] = w[0] * iw[1] - w[1] * iw[0];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {   // per-axis inertia
+                a_w[k] = dt * (tau[k] - gy[k]);
+                dww[k] = fq(a_w[k], A.u.I[k], A.u.rI[k], I_ok, m_ga & ev & !flk);
+            }
+        }
+        if (__any_sync(0xffffffffu, slow)) {
+            if (slow) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    dvv[k] = div_ieee(a_v[k], m);
+                    dww[k] = div_ieee(a_w[k], A.u.I[k]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            add_if(!pl, v[k], dvv[k]);
+            add_if(!flk, w[k], dww[k]);
+        }
+        // drivers overwrite after the update
+        if (drp >= 0)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) v[k] = dvel[k];
+        if (drf >= 0) {
+            w[0] = Real(0.0);
+            w[1] = Real(0.0);
+            w[2] = drot;
+        }
+
+        // ============ constraint iterations (_core.pyx:1069-1076) ============
+        Real nP[2][3], bP[2];   // the phase's element tangent, negated on the b side
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            bP[c] = a_side[c] ? bias : bias_l;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) nP[c][k] = a_side[c] ? nn[k] : -nn_l[k];
+        }
+        // (rods without distance-projected elements and bindings: no sweeps,
+        // like the general kernel)
+        int vb_off = HL_VA;
+        const int iters = (BIND || A.any_dist) ? A.iters : 0;
+        if (iters > 0) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+            __syncthreads();
+        }
+        int rem = Rg;   // radius still to come after the current phase
+        for (int it = iters; it > 0; --it) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                --rem;
+                const bool chk = pv && dout <= rem;
+                Real dv[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) dv[k] = HS(vb_off + k, partner[c]) - v[k];
+                Real x = dv[0] * nP[c][0];
+                x = x + dv[1] * nP[c][1];
+                x = x + dv[2] * nP[c][2];
+                x = x + bP[c];
+                const Real q0 = (-x) * rwsP[c];
+                Real lam = fma(fma(-q0, wsP[c], -x), rwsP[c], q0);
+                const bool z = is_zero(x);
+                if (z) lam = Real(-0.0);
+                ok = ok & !(chk & actP[c] & !(in_window(x) | z));
+#pragma unroll
+                for (int k = 0; k < 3; ++k) sub_if(actP[c], v[k], im * lam * nP[c][k]);
+                vb_off = HL_VA + HL_VB - vb_off;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+                __syncthreads();
+            }
+            if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
+                Real vrel = Real(0.0);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) vrel = vrel + (HS(vb_off + k, t_b) - v[k]) * bn[k];
+                bool lok = true;
+                const Real lam = hl_quot(-(vrel + bbias), bws, brws, lok);
+                ok = ok & (!(bact & (dout <= rem)) | lok);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * lam * bn[k]);
+                vb_off = HL_VA + HL_VB - vb_off;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+                __syncthreads();
+            }
+        }
+
+        // ================= integrate (_core.pyx:1023-1042) =================
+#pragma unroll
+        for (int k = 0; k < 3; ++k) p[k] = p[k] + dt * v[k];
+        {
+            Real dq[4];
+            const Real om[4] = {Real(0.0), w[0], w[1], w[2]};
+            hprod(q, om, dq);
+            const Real h = dt * Real(0.5);
+            Real qq4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) qq4[k] = q[k] + h * dq[k];
+            const Real qq = qq4[0] * qq4[0] + qq4[1] * qq4[1] + qq4[2] * qq4[2] + qq4[3] * qq4[3];
+            const bool qq_ok = in_window(qq);
+            ok = ok & (!(own & ev) | qq_ok);
+            const Real nrm = sqrt_rn(qq);
+            const Real rn = rcp_rn(nrm);
+            Real qn[4];
+            hl_div<4>(qq4, nrm, rn, qq_ok, own & ev, qn);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = qn[k];
+        }
+
+        // ===== exchange: owned state into this CTA's and the neighbours' next buffer =====
+        if (GX && step + 1 < A.steps) {
+            const int par = step & 1;
+            Real* mine = A.halo + (size_t(par) * ncl + rank) * 2 * hrec;
+            auto gput = [&](Real* b, int idx) {
+                Real* x = b + (size_t(r) * G + idx) * HL_NSTATE;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    x[HL_P + k] = p[k];
+                    x[HL_V + k] = v[k];
+                    x[HL_W + k] = w[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[HL_Q + k] = q[k];
+            };
+            if (push_l) gput(mine, i - tk.o0);                    // side 0: for the left neighbour
+            if (push_r) gput(mine + hrec, i - (tk.o1 - G));       // side 1: for the right one
+            __syncthreads();
+            if (t == 0) {
+                __threadfence();
+                st_release_gpu(A.flags + rank, step + 1);
+                if (has_l)
+                    while (ld_acquire_gpu(A.flags + rank - 1) < step + 1) {}
+                if (has_r)
+                    while (ld_acquire_gpu(A.flags + rank + 1) < step + 1) {}
+            }
+            __syncthreads();
+            if (pv && !own) {
+                const bool left = i < tk.o0;
+                const Real* src = A.halo + (size_t(par) * ncl + (left ? rank - 1 : rank + 1)) * 2 * hrec +
+                                  (left ? hrec : 0);
+                const int idx = left ? i - (tk.o0 - G) : i - tk.o1;
+                const Real* x = src + (size_t(r) * G + idx) * HL_NSTATE;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    p[k] = ld_halo(x + HL_P + k);
+                    v[k] = ld_halo(x + HL_V + k);
+                    w[k] = ld_halo(x + HL_W + k);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) q[k] = ld_halo(x + HL_Q + k);
+            }
+            cur ^= 1;
+        } else if (!GX && step + 1 < A.steps) {
+            cur ^= 1;
+            const int nb = cur * HL_NSTATE;
+            auto put = [&](Real* base, int x) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    base[(nb + HL_P + k) * T + x] = p[k];
+                    base[(nb + HL_V + k) * T + x] = v[k];
+                    base[(nb + HL_W + k) * T + x] = w[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) base[(nb + HL_Q + k) * T + x] = q[k];
+            };
+            if (own) put(sm, t);
+            if (push_l) put(sm_l, t_l);
+            if (push_r) put(sm_r, t_r);
+            if (ncl > 1) cluster_barrier();
+            else __syncthreads();
+        }
+    }
+
+    // ---- the cluster's vote, then write-back (or the exact redo) ----
+    int* vote = reinterpret_cast<int*>(smem_raw + align16(size_t(HL_NF) * size_t(T) * sizeof(Real)));
+    const int bad = __syncthreads_or(!ok);   // (ok only collects results the owned range needs)
+    int any = 0;
+    if constexpr (GX) {
+        // grid: OR into the redo word, then an arrival count over all CTAs
+        // (co-resident) before anyone reads it
+        if (t == 0) {
+            if (bad) atomicOr(A.redo_count, 1);
+            __threadfence();
+            atomicAdd(A.flags + ncl, 1);
+            while (ld_acquire_gpu(A.flags + ncl) < int(ncl)) {}
+            *vote = ld_acquire_gpu(A.redo_count);
+        }
+        __syncthreads();
+        any = *vote;
+        if (any) return;
+    } else {
+        if (t == 0) *vote = bad;
+        cluster_barrier();
+        if (t < int(ncl)) any = *cg::this_cluster().map_shared_rank(vote, t);
+        any = __syncthreads_or(any);
+        cluster_barrier();   // every remote read done before a CTA exits
+    }
+    if (any) {   // (a one-CTA group's exact launch steps the listed task 0)
+        if (rank == 0 && t == 0) {
+            A.redo_list[0] = 0;
+            *A.redo_count = 1;
+        }
+        return;
+    }
+    if (own) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            A.pos[3 * size_t(pt) + k] = p[k];
+            A.vel[3 * size_t(pt) + k] = v[k];
+        }
+        if (ev) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) A.w[3 * size_t(el) + k] = w[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) A.q[4 * size_t(el) + k] = q[k];
+        }
+    }
+#undef HS
+}
+
+}  // namespace rsb

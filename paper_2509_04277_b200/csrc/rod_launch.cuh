@@ -11,6 +11,7 @@
 #include "rod_step.cuh"
 #if !RSB_FEAT
 #include "rod_batch.cuh"
+#include "rod_halo.cuh"
 #include "rod_warp.cuh"
 #endif
 
@@ -298,6 +299,82 @@ cudaError_t warp_step(int gen, int form, const StepArgs<Real>* a, int grid, cuda
     switch (form) {
         case 1: return gen ? warp_one<Real, true, 1>(a, grid, st) : warp_one<Real, false, 1>(a, grid, st);
         case 2: return gen ? warp_one<Real, true, 2>(a, grid, st) : warp_one<Real, false, 2>(a, grid, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// The wide-halo cluster kernel (rod_halo.cuh): one cluster of ncta CTAs.
+template <typename Real, bool GEN, bool BIND, int TB, bool GX>
+static cudaError_t halo_one(int what, const StepArgs<Real>* a, int ncta, int threads, cudaStream_t st, int* out) {
+    auto fn = rod_halo_kernel<Real, RSB_MODE_ID, GEN, BIND, TB, GX>;
+    static std::atomic<bool> done[64];
+    cudaError_t e = configure_once(fn, done);
+    if (e != cudaSuccess) return e;
+    if constexpr (GX) {   // co-resident grid (cooperative launch)
+        const size_t smem = halo_smem_bytes(threads, sizeof(Real));
+        if (what == 1) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, threads, smem);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ncta);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fn, *a);
+    }
+    if (ncta > 8) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncta);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = halo_smem_bytes(threads, sizeof(Real));
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncta;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    if (what == 1) {
+        cfg.numAttrs = 1;
+        return cudaOccupancyMaxActiveClusters(out, (void*)fn, &cfg);
+    }
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, fn, *a);
+}
+// what: 0 launch, 1 occupancy query (cluster: active clusters, grid: CTAs
+// per SM); tb: 256 or 512; gx: grid exchange instead of one cluster
+template <typename Real>
+cudaError_t halo_step(int what, int gen, int bind, int tb, int gx, const StepArgs<Real>* a, int ncta, int threads,
+                      cudaStream_t st, int* out) {
+    const int sel = (gen ? 1 : 0) | (bind ? 2 : 0) | (tb > 256 ? 4 : 0) | (gx ? 8 : 0);
+    switch (sel) {
+#define RSB_H(S, G, B, T, X) \
+    case S: return halo_one<Real, G, B, T, X>(what, a, ncta, threads, st, out);
+        RSB_H(0, false, false, 256, false)
+        RSB_H(1, true, false, 256, false)
+        RSB_H(2, false, true, 256, false)
+        RSB_H(3, true, true, 256, false)
+        RSB_H(4, false, false, 512, false)
+        RSB_H(5, true, false, 512, false)
+        RSB_H(6, false, true, 512, false)
+        RSB_H(7, true, true, 512, false)
+        RSB_H(8, false, false, 256, true)
+        RSB_H(9, true, false, 256, true)
+        RSB_H(10, false, true, 256, true)
+        RSB_H(11, true, true, 256, true)
+        RSB_H(12, false, false, 512, true)
+        RSB_H(13, true, false, 512, true)
+        RSB_H(14, false, true, 512, true)
+        RSB_H(15, true, true, 512, true)
+#undef RSB_H
     }
     return cudaErrorInvalidValue;
 }

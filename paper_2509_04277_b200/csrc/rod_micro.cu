@@ -175,6 +175,43 @@ __global__ void nb_sync_kernel(double* out, int iters) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Neighbour-only exchange across a co-resident grid (the wide-halo kernel's
+// grid exchange, rod_halo.cuh): per round every CTA writes a halo word,
+// bar.sync, thread 0 fences, publishes its flag (release.gpu) and acquires
+// both neighbours', bar.sync, then reads the neighbour's word through L2.
+__global__ void grid_flag_kernel(double* out, int* flags, double* halo, int iters) {
+    const int rank = blockIdx.x, n = gridDim.x;
+    const bool has_l = rank > 0, has_r = rank + 1 < n;
+    double acc = 0;
+    __syncthreads();
+    const uint64_t t0 = gtimer();
+    const long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        if (threadIdx.x == 0) halo[2 * rank + (it & 1) * 2 * n] = double(it);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flags + rank), "r"(it + 1) : "memory");
+            int v;
+            if (has_l)
+                do asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + rank - 1) : "memory");
+                while (v < it + 1);
+            if (has_r)
+                do asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + rank + 1) : "memory");
+                while (v < it + 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && has_r) acc += __ldcg(halo + 2 * (rank + 1) + (it & 1) * 2 * n);
+    }
+    const long long c1 = clock64();
+    const uint64_t t1 = gtimer();
+    if (rank == 0 && threadIdx.x == 0) {
+        out[0] = double(c1 - c0) / iters;
+        out[1] = double(t1 - t0) / iters;
+    }
+    if (acc == -1.0) out[2] = acc;
+}
+
 // DSMEM dependent remote load latency (thread 0 of rank 0 chases through
 // rank 1's shared memory)
 __global__ void dsmem_kernel(double* out, int iters) {
@@ -203,7 +240,9 @@ __global__ void dsmem_kernel(double* out, int iters) {
 
 // kind: 0 DADD, 1 DMUL, 2 DFMA, 3 IEEE div, 4 sqrt(+add), 5 div_rn, 6 1/x
 //       (chains; param unused), 7 LDS chase, 8 bar.sync (param = threads),
-//       9 cluster barrier (param = CTAs), 10 DSMEM chase (2-CTA cluster)
+//       9 cluster barrier (param = CTAs), 10 DSMEM chase (2-CTA cluster),
+//       11 neighbour mbarrier sync (param = CTAs), 12 grid neighbour flag
+//       exchange (param = CTAs)
 cudaError_t run(int kind, int param, double* res) {
     double* buf = nullptr;
     cudaError_t e = cudaMalloc(&buf, 4 * sizeof(double));
@@ -243,6 +282,22 @@ cudaError_t run(int kind, int param, double* res) {
                     return cudaLaunchKernelEx(&cfg, cluster_bar_kernel, buf, iters);
                 }
                 return cudaLaunchKernelEx(&cfg, dsmem_kernel, buf, iters);
+            }
+            case 12: {   // grid neighbour exchange, param CTAs (co-resident)
+                int* flags = nullptr;
+                double* halo = nullptr;
+                cudaError_t e2 = cudaMalloc(&flags, sizeof(int) * param);
+                if (e2 == cudaSuccess) e2 = cudaMalloc(&halo, sizeof(double) * 4 * param);
+                if (e2 == cudaSuccess) e2 = cudaMemset(flags, 0, sizeof(int) * param);
+                if (e2 == cudaSuccess) {
+                    int it = iters;
+                    void* args[] = {&buf, &flags, &halo, &it};
+                    e2 = cudaLaunchCooperativeKernel((const void*)grid_flag_kernel, dim3(param), dim3(128), args, 0, nullptr);
+                }
+                if (e2 == cudaSuccess) e2 = cudaDeviceSynchronize();
+                cudaFree(flags);
+                cudaFree(halo);
+                return e2;
             }
             default: return cudaErrorInvalidValue;
         }

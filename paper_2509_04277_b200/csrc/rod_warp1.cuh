@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(32, 1) rod_warp1_kernel(const StepArgs<Real> A
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 f[k] = m * grav[k];
-                f[k] = f[k] + (GEN ? A.fext[3 * size_t(pt) + k] : Real(0));
+                f[k] = f[k] + ((GEN && A.has_fext) ? A.fext[3 * size_t(pt) + k] : Real(0));
                 const Real g0 = f[k] + ef[k];   // the point's own element (not the last point)
                 f[k] = ev ? g0 : f[k];
                 const Real g = f[k] - efl[k];

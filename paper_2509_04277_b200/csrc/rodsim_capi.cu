@@ -25,6 +25,7 @@
 #include "../../include/rodsim_b200.h"
 #include "rod_common.h"
 #include "rod_batch.cuh"
+#include "rod_halo.cuh"
 #include "rod_warp.cuh"
 #include "rod_step.cuh"
 
@@ -40,6 +41,8 @@
     cudaError_t batch_step(int, int, const StepArgs<Real>*, int, cudaStream_t, int*);             \
     template <typename Real>                                                                       \
     cudaError_t warp_step(int, int, const StepArgs<Real>*, int, cudaStream_t);                    \
+    template <typename Real>                                                                       \
+    cudaError_t halo_step(int, int, int, int, int, const StepArgs<Real>*, int, int, cudaStream_t, int*); \
     }                                                                                              \
     }
 RSB_DECLARE_MODE(mirror)
@@ -138,6 +141,18 @@ struct Group {       // one kernel launch
     int rw_form = 0;                // 1: every rod <= 31 elements (one point per lane),
                                     // 2: 32..63 (two per lane)
     int bw_grid = 0;
+    // cluster groups of one rod or two rods bound point to point at the same
+    // local index: the wide-halo kernel (rod_halo.cuh) takes the speculative
+    // launch -- one cluster barrier per step instead of one per phase
+    bool halo = false;
+    bool h_gen = false, h_bind = false;
+    int h_cta = 0, h_threads = 0, h_tb = 256, h_w = 0, h_g = 0, h_nr = 0, h_np = 0, h_iters = 0;
+    int32_t h_poff[2] = {0, 0}, h_eoff[2] = {0, 0};
+    bool h_gx = false;              // grid exchange (co-resident grid) instead of one cluster
+    std::vector<HaloTask> h_tasks;
+    HaloTask* d_htask = nullptr;
+    int32_t* d_hflags = nullptr;    // grid exchange: per-CTA step flags + arrival count
+    void* d_hhalo = nullptr;        // grid exchange: (2, C, 2, NR, G, 13) halo records
 };
 
 // groups with speculative kernels: the batched stream variant and the
@@ -146,6 +161,7 @@ struct Group {       // one kernel launch
 // torques carry rounding noise (~1e-300) below the fast path's window, and
 // a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
 constexpr int kSpecMinSteps = 32;
+constexpr int kHaloCtaMinPoints = 100;
 constexpr int kSpecBackoff = 64;
 bool spec_group(const Group& g) {
     return (g.tier == TIER_STREAM && g.variant == 7) || (g.tier == TIER_CTA && g.variant == 0);
@@ -179,6 +195,11 @@ struct rs_handle_s {
     bool bw_on = true;              // warp-per-rod batched kernel (RSB_BW=0: off)
     bool rw_on = true;              // one-warp single-rod kernel (RSB_RW=0: off)
     bool rw1_on = true;             // its one-point-per-lane form (RSB_RW1=0: off)
+    bool halo_on = true;            // wide-halo cluster kernel (RSB_HALO=0: off)
+    int halo_ctas = 0;              // its CTA count (RSB_HALO_CTAS; 0: the planner's)
+    int halo_grid = -1;             // RSB_HALO_GRID: 1 grid exchange, 0 cluster only, -1 the planner's
+    int halo_width = 128;           // RSB_HALO_W: target threads per CTA of the grid exchange
+    int halo_cta = -1;              // RSB_HALO_CTA: one-CTA segments (-1: from kHaloCtaMinPoints)
     int bw_shape = -1;              // its launch shape (RSB_BW_SHAPE, kBwShapes; -1: the planner's)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
     bool last_spec = false;         // the last launch speculated (rs_last_redo_count)
@@ -198,6 +219,8 @@ struct rs_handle_s {
     DevBuf pos, vel, q, w;
     DevBuf rest, ustar, inert, ks, kp, gt, gr, kb, mass, invm, fext, drv_v, drv_rot;
     DevBuf pflags, pt_elem, tasks, binds, drvs, grabs;
+    DevBuf hdrv, hbind;             // wide-halo kernel: per-point driver rods, binding codes
+    std::vector<int32_t> h_hdrv, h_hbind;
     // mesh contacts: tree + mesh (static), contact slots (state)
     DevBuf nmin, nmax, verts, nstart, ncount, torder, tris, cradii, cmask;
     DevBuf cact, cnorm, cdepth, cacc_n, cacc_t;
@@ -443,6 +466,180 @@ bool elem_consts_equal(const rs_world_desc& d, int64_t a, int64_t b) {
     return true;
 }
 
+int halo_query(rs_handle h, const Group& g, int* out);
+
+// Wide-halo kernel (rod_halo.cuh) for cluster groups: one rod, or two rods of
+// equal length bound point to point at the same local index (a matching), with
+// the structural flags of World rods (junctions inside a rod, colours by local
+// index), launch-uniform material constants and no scene features.  Each CTA
+// owns ~np / C consecutive local indices plus G = 2I + 1 ghost points per
+// side; the planner takes the largest cluster (<= 16) whose CTAs own at least
+// G points each.
+int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vector<int32_t>& pt_elem) {
+    const rs_world_desc& d = h->d;
+    const int64_t P = d.P;
+    h->h_hdrv.assign(size_t(2 * P), -1);
+    h->h_hbind.assign(size_t(P), -1);
+    for (int64_t r = 0; r < d.R; ++r) {   // rod order: the last rod driving a point wins
+        if (d.drv_pt[r] >= 0 && d.drv_pt[r] < P) h->h_hdrv[size_t(2 * d.drv_pt[r])] = int32_t(r);
+        if (d.drv_fr[r] >= 0 && d.drv_fr[r] < d.E) h->h_hdrv[size_t(2 * d.elem_point[d.drv_fr[r]] + 1)] = int32_t(r);
+    }
+    for (Group& g : h->groups) {
+        g.halo = false;
+        // one-CTA segments (a single task) of >= kHaloCtaMinPoints points:
+        // spread over a cluster as well (cfg4, K = 100: 128 elements 4.31 ->
+        // 3.93 us/step, 256: 6.23 -> 3.97, 512: 9.59 -> 4.06; the 64-element
+        // cantilever stays on its CTA, 3.80 vs 3.91).  RSB_HALO_CTA: 0 never,
+        // 1 at any size
+        const bool cta_ok = g.tier == TIER_CTA && g.ncta == 1 && h->halo_cta != 0 &&
+                            (h->halo_cta == 1 || h->h_tasks[g.task_begin].np >= kHaloCtaMinPoints);
+        if ((g.tier != TIER_CLUSTER && g.tier != TIER_GRID && !cta_ok) || g.uni != 2 || !h->halo_on ||
+            h->contacts_on || d.has_self || d.live || d.force_ctas > 0 || d.force_variant >= 0)
+            continue;
+        const CtaTask& tf = h->h_tasks[g.task_begin];
+        const CtaTask& tl = h->h_tasks[g.task_begin + g.ncta - 1];
+        const int64_t p0 = tf.p0, p1 = int64_t(tl.p0) + tl.np;
+        const int64_t r0 = rod_of(d, p0), r1 = rod_of(d, p1 - 1);
+        const int nr = int(r1 - r0 + 1);
+        if (nr > 2 || d.rod_offsets[r0] != p0 || d.rod_offsets[r1 + 1] != p1) continue;
+        const int64_t np = d.rod_offsets[r0 + 1] - d.rod_offsets[r0];
+        if (nr == 2 && d.rod_offsets[r1 + 1] - d.rod_offsets[r1] != np) continue;
+        bool ok = true, gen = false;
+        for (int64_t r = r0; r <= r1 && ok; ++r) {
+            const int64_t o = d.rod_offsets[r];
+            const int64_t ne = np - 1;
+            for (int64_t j = 0; j < np && ok; ++j) {
+                const uint32_t f = pflags[size_t(o + j)];
+                const uint32_t want = (j < ne ? uint32_t(SF_HAS_ELEM) : 0u) | (j > 0 ? uint32_t(SF_HAS_PREV) : 0u) |
+                                      (j < ne - 1 ? uint32_t(SF_JVALID) : 0u) |
+                                      (j > 0 && j < ne ? uint32_t(SF_JPREV) : 0u) |
+                                      (j < ne && (j & 1) ? uint32_t(SF_PARITY) : 0u);
+                const uint32_t mask = SF_HAS_ELEM | SF_HAS_PREV | SF_JVALID | SF_JPREV | SF_PARITY;
+                ok = (f & mask) == want && pt_elem[size_t(o + j)] == (j < ne ? int32_t(o + j - r) : -1);
+                gen |= (f & SF_EXT) != 0;
+            }
+        }
+        // bindings of the segment: across the two rods, same local index, a matching
+        bool bind = false;
+        std::vector<uint8_t> used;
+        for (int64_t k = 0; k < d.nbind && ok; ++k) {
+            const int64_t a = d.bind_a[k], b = d.bind_b[k];
+            const bool ina = a >= p0 && a < p1, inb = b >= p0 && b < p1;
+            if (!ina && !inb) continue;
+            const int64_t ra = rod_of(d, a), rb = rod_of(d, b);
+            if (nr != 2 || ra == rb || a - d.rod_offsets[ra] != b - d.rod_offsets[rb]) {
+                ok = false;
+                break;
+            }
+            if (used.empty()) used.assign(size_t(p1 - p0), 0);
+            if (used[size_t(a - p0)] || used[size_t(b - p0)]) {
+                ok = false;
+                break;
+            }
+            used[size_t(a - p0)] = used[size_t(b - p0)] = 1;
+            bind = true;
+        }
+        if (!ok) continue;
+        // ghost width: the step's dependency radius (scatter 1, gather 1,
+        // one per colour phase; without distance-projected elements or
+        // bindings there are no sweeps)
+        const int G = (g.any_dist || bind) ? int(2 * d.iters + 1) : 1;
+        // one cluster of up to 16 CTAs while its CTAs stay within 256
+        // threads (no spills); beyond, or on request, a co-resident grid of
+        // CTAs of ~halo_width threads (more, thinner CTAs: a phase's issue
+        // per SM is what bounds its latency)
+        const int m_cl = int((np + kMaxCluster - 1) / kMaxCluster);
+        bool gx = h->halo_grid == 1 || (h->halo_grid != 0 && nr * (m_cl + 2 * G) > 256);
+        int C;
+        if (!gx) {
+            C = h->halo_ctas > 0 ? h->halo_ctas : kMaxCluster;
+            C = std::min(C, kMaxCluster);
+        } else {
+            // (wider CTAs once the grid passes ~96 CTAs: cfg4 N = 16384 at
+            // 128 / 192 / 256 threads: 10.7 / 9.7 / 9.5 us per step)
+            int width = h->halo_width;
+            auto ctas_for = [&](int wdt) {
+                const int m_t = std::max(G, wdt / nr - 2 * G);
+                return int((np + m_t - 1) / m_t);
+            };
+            while (h->halo_ctas <= 0 && ctas_for(width) > 96 && width < 256) width += 32;
+            C = h->halo_ctas > 0 ? h->halo_ctas : ctas_for(width);
+            C = std::min(C, h->num_sms > 0 ? h->num_sms : 148);
+        }
+        C = int(std::min<int64_t>(C, np / G));
+        if (C < 1) continue;
+        auto layout = [&](int c, std::vector<HaloTask>& ts, int& wmax) {
+            ts.clear();
+            wmax = 0;
+            const int64_t base = np / c, rem = np % c;
+            int64_t o = 0;
+            for (int k = 0; k < c; ++k) {
+                const int64_t sz = base + (k < rem ? 1 : 0);
+                HaloTask t{};
+                t.o0 = int32_t(o);
+                t.o1 = int32_t(o + sz);
+                t.x0 = int32_t(std::max<int64_t>(0, o - G));
+                t.x1 = int32_t(std::min<int64_t>(np, o + sz + G));
+                wmax = std::max(wmax, int(t.x1 - t.x0));
+                ts.push_back(t);
+                o += sz;
+            }
+        };
+        std::vector<HaloTask> ts;
+        int wmax = 0;
+        layout(C, ts, wmax);
+        const int threads = (nr * wmax + 31) / 32 * 32;
+        if (threads > 512) continue;
+        g.h_tasks = ts;
+        g.h_gx = gx;
+        g.h_cta = C;
+        g.h_w = wmax;
+        g.h_threads = threads;
+        g.h_tb = threads > 256 ? 512 : 256;
+        g.h_g = G;
+        g.h_iters = int(d.iters);
+        g.h_nr = nr;
+        g.h_np = int(np);
+        g.h_gen = gen;
+        g.h_bind = bind;
+        for (int r = 0; r < 2; ++r) {
+            const int64_t rr = std::min<int64_t>(r0 + r, r1);
+            g.h_poff[r] = int32_t(d.rod_offsets[rr]);
+            g.h_eoff[r] = int32_t(d.rod_offsets[rr] - rr);
+        }
+        if (bind)
+            for (int64_t k = 0; k < d.nbind; ++k) {
+                const int64_t a = d.bind_a[k], b = d.bind_b[k];
+                if (a < p0 || a >= p1) continue;
+                const int32_t mode = d.bind_mode[k] != 0 ? 2 : 0;
+                h->h_hbind[size_t(a)] = 1 | mode;
+                h->h_hbind[size_t(b)] = mode;
+            }
+        if (h->dry) {
+            g.halo = true;
+            continue;
+        }
+        int occ = 0;
+        int rc = halo_query(h, g, &occ);
+        if (rc) return rc;
+        if (occ < 1 || (gx && int64_t(occ) * h->num_sms < C)) continue;
+        if (gx) {
+            CK(cudaMalloc(&g.d_hflags, sizeof(int32_t) * size_t(C + 1)));
+            const size_t words = size_t(2) * C * 2 * nr * G * HL_NSTATE;
+            CK(cudaMalloc(&g.d_hhalo, h->rsz * words));
+        }
+        CK(cudaMalloc(&g.d_htask, sizeof(HaloTask) * ts.size()));
+        CK(cudaMemcpy(g.d_htask, ts.data(), sizeof(HaloTask) * ts.size(), cudaMemcpyHostToDevice));
+        if (!h->redo_count.p || !h->redo_list.p) {   // (a one-CTA group's exact launch reads the list)
+            int rc2 = dev_alloc(h->redo_count, sizeof(int32_t));
+            if (!rc2 && !h->redo_list.p) rc2 = dev_alloc(h->redo_list, sizeof(int32_t));
+            if (rc2) return rc2;
+        }
+        g.halo = true;
+    }
+    return RS_OK;
+}
+
 int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_elem) {
     const rs_world_desc& d = h->d;
     const int64_t P = d.P, R = d.R;
@@ -561,6 +758,9 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
     for (Group& g : h->groups) {
         if (g.d_flags) cudaFree(g.d_flags);
         if (g.d_halo) cudaFree(g.d_halo);
+        if (g.d_htask) cudaFree(g.d_htask);
+        if (g.d_hflags) cudaFree(g.d_hflags);
+        if (g.d_hhalo) cudaFree(g.d_hhalo);
     }
     h->h_tasks.clear();
     h->h_binds.clear();
@@ -968,6 +1168,8 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
               ((h->groups[0].tier == TIER_CTA && h->groups[0].ncta == 1 && h->groups[0].variant <= 4 &&
                 h->groups[0].variant != 3) ||
                h->groups[0].tier == TIER_CLUSTER);
+    int rc_h = plan_halo(h, pflags, pt_elem);
+    if (rc_h) return rc_h;
     h->planned = true;
     return RS_OK;
 }
@@ -1127,6 +1329,8 @@ int upload_static(rs_handle h) {
     if ((rc = put_u8(h, h->cmask, d.cmask, P))) return rc;
     if ((rc = put_vec(h, h->binds, h->h_binds))) return rc;
     if ((rc = put_vec(h, h->drvs, h->h_drvs))) return rc;
+    if ((rc = put_vec(h, h->hdrv, h->h_hdrv))) return rc;
+    if ((rc = put_vec(h, h->hbind, h->h_hbind))) return rc;
     return build_grabs(h);
 }
 
@@ -1353,7 +1557,34 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.gy = Real(h->d.gy);
     a.gz = Real(h->d.gz);
     a.bar_cycles = h->bar_timing ? h->d_bar : nullptr;
+    a.htask = g.d_htask;
+    a.hdrv = static_cast<const int32_t*>(h->hdrv.p);
+    a.hbind = static_cast<const int32_t*>(h->hbind.p);
+    a.h_nr = g.h_nr;
+    a.h_np = g.h_np;
+    a.h_w = g.h_w;
+    a.h_g = g.h_g;
+    for (int r = 0; r < 2; ++r) {
+        a.h_poff[r] = g.h_poff[r];
+        a.h_eoff[r] = g.h_eoff[r];
+    }
     return a;
+}
+
+int halo_query(rs_handle h, const Group& g, int* out) {
+    cudaError_t e;
+    const int gen = g.h_gen ? 1 : 0, bind = g.h_bind ? 1 : 0;
+    if (h->prec == RS_F64_MIRROR)
+        e = mirror::halo_step<double>(1, gen, bind, g.h_tb, g.h_gx, nullptr, g.h_cta, g.h_threads, nullptr, out);
+    else if (h->prec == RS_F32)
+        e = f32::halo_step<float>(1, gen, bind, g.h_tb, g.h_gx, nullptr, g.h_cta, g.h_threads, nullptr, out);
+    else
+        e = f64fast::halo_step<double>(1, gen, bind, g.h_tb, g.h_gx, nullptr, g.h_cta, g.h_threads, nullptr, out);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;   // not launchable here: the group keeps the general kernel
+    }
+    return RS_OK;
 }
 
 // Launch one group, or (t_cnt >= 0, CTA/stream tiers only) the task
@@ -1478,6 +1709,53 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         auto a = go(make_args<double>(h, g, step0, steps));
         return f64fast::warp_step<double>(gen, g.rw_form, &a, nt, h->st);
     };
+    // the wide-halo kernel takes the launch of an eligible cluster group
+    // (no grabs, not live, ghost width still covering the iterations); the
+    // exact general kernel follows in consume mode and runs only if the
+    // halo launch's vote failed
+    const bool halo = g.halo && h->halo_on && h->h_grabs.empty() && !h->live && cfg0 < 3 &&
+                      (g.h_g == 1 || 2 * h->d.iters + 1 <= g.h_g) &&
+                      h->redo_count.p && t_cnt < 0;
+    if (halo) {
+        CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
+        if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 1), h->st));
+        const int gen = (g.h_gen || h->has_fext) ? 1 : 0, bind = g.h_bind ? 1 : 0;
+        auto go = [&](auto a) {
+            a.redo_count = static_cast<int32_t*>(h->redo_count.p);
+            a.redo_list = static_cast<int32_t*>(h->redo_list.p);
+            a.redo_mode = 1;
+            return a;
+        };
+        // the halo launch's own exchange buffers (the general kernel keeps its own)
+        auto hx = [&](auto a) {
+            a.flags = g.d_hflags;
+            a.halo = static_cast<decltype(a.halo)>(g.d_hhalo);
+            return a;
+        };
+        cudaError_t eh;
+        if (h->prec == RS_F64_MIRROR) {
+            auto a = go(make_args<double>(h, g, step0, steps));
+            auto ah = hx(a);
+            eh = mirror::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &ah, g.h_cta, g.h_threads, h->st, nullptr);
+            if (eh == cudaSuccess) eh = mirror::launch_step<double>(g.variant, g.tier, cfg0, a, grid, g.threads, g.smem, g.cluster, h->st);
+        } else if (h->prec == RS_F32) {
+            auto a = go(make_args<float>(h, g, step0, steps));
+            auto ah = hx(a);
+            eh = f32::halo_step<float>(0, gen, bind, g.h_tb, g.h_gx, &ah, g.h_cta, g.h_threads, h->st, nullptr);
+            if (eh == cudaSuccess) eh = f32::launch_step<float>(g.variant, g.tier, cfg0, a, grid, g.threads, g.smem, g.cluster, h->st);
+        } else {
+            auto a = go(make_args<double>(h, g, step0, steps));
+            auto ah = hx(a);
+            eh = f64fast::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &ah, g.h_cta, g.h_threads, h->st, nullptr);
+            if (eh == cudaSuccess) eh = f64fast::launch_step<double>(g.variant, g.tier, cfg0, a, grid, g.threads, g.smem, g.cluster, h->st);
+        }
+        if (eh != cudaSuccess)
+            return fail(RS_E_CUDA, "wide-halo launch (%d CTAs x %d threads) failed: %s", g.h_cta, g.h_threads,
+                        cudaGetErrorString(eh));
+        h->last_spec = true;
+        h->launches += 2;
+        return RS_OK;
+    }
     cudaError_t e = bw ? one_bw() : rw ? one_rw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
     if (e == cudaSuccess && spec) e = one(cfg0, 1);
     if (e == cudaSuccess && spec && backoff && !h->redo_ev_live[gi]) {
@@ -1651,6 +1929,11 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     h->step = desc->step_index;
     if (const char* dbg = getenv("RSB_DEBUG")) h->debug = atoi(dbg);
     if (const char* sp = getenv("RSB_SPEC")) h->spec = atoi(sp) != 0;
+    if (const char* e = getenv("RSB_HALO")) h->halo_on = atoi(e) != 0;
+    if (const char* e = getenv("RSB_HALO_CTAS")) h->halo_ctas = atoi(e);
+    if (const char* e = getenv("RSB_HALO_GRID")) h->halo_grid = atoi(e);
+    if (const char* e = getenv("RSB_HALO_W")) h->halo_width = std::max(64, atoi(e));
+    if (const char* e = getenv("RSB_HALO_CTA")) h->halo_cta = atoi(e);
     if (const char* sp = getenv("RSB_BW")) h->bw_on = atoi(sp) != 0;
     if (const char* sp = getenv("RSB_RW")) h->rw_on = atoi(sp) != 0;
     if (const char* sp = getenv("RSB_RW1")) h->rw1_on = atoi(sp) != 0;
@@ -1978,11 +2261,14 @@ void rs_destroy(rs_handle h) {
                       &h->nstart, &h->ncount, &h->torder, &h->tris, &h->cradii, &h->cmask, &h->cact, &h->cnorm,
                       &h->cdepth, &h->cacc_n, &h->cacc_t, &h->grp_rod, &h->grp_gi, &h->grp_s, &h->grp_e,
                       &h->grp_c, &h->gp_count, &h->pair_a, &h->pair_b, &h->pair_md, &h->pair_acc, &h->g_act_d, &h->g_pt_d,
-                      &h->g_tgt_d, &h->redo_list, &h->redo_count})
+                      &h->g_tgt_d, &h->redo_list, &h->redo_count, &h->hdrv, &h->hbind})
         if (b->p) cudaFree(b->p);
     for (Group& g : h->groups) {
         if (g.d_flags) cudaFree(g.d_flags);
         if (g.d_halo) cudaFree(g.d_halo);
+        if (g.d_htask) cudaFree(g.d_htask);
+        if (g.d_hflags) cudaFree(g.d_hflags);
+        if (g.d_hhalo) cudaFree(g.d_hhalo);
     }
     for (void* p : h->registered) cudaHostUnregister(p);
     for (cudaEvent_t e : h->redo_ev)
@@ -2099,17 +2385,27 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
             snprintf(bwj, sizeof bwj, "{\"shape\": %d, \"warps_per_cta\": %d, \"grid\": %d, \"shared_statics\": %s, \"general\": %s}",
                      g.bw_shape, kBwShapes[g.bw_shape].wpc, g.bw_grid, kBwShapes[g.bw_shape].shst ? "true" : "false",
                      g.bw_gen ? "true" : "false");
-        char tmp[900];
+        // the wide-halo cluster kernel (rod_halo.cuh) that takes the
+        // group's launches: CTAs, threads, ghost width; one cluster barrier
+        // per step, the phases' barriers CTA-local
+        char hj[200] = "null";
+        if (g.halo)
+            snprintf(hj, sizeof hj, "{\"ctas\": %d, \"threads\": %d, \"ghost\": %d, \"rods\": %d, \"bindings\": %s, "
+                     "\"exchange\": \"%s\"}",
+                     g.h_cta, g.h_threads, g.h_g, g.h_nr, g.h_bind ? "true" : "false", g.h_gx ? "grid" : "cluster");
+        char tmp[1200];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "
                  "\"uniform\": %s, \"ctas\": %d, \"grid\": %d, \"threads\": %d, \"cluster\": %d, "
                  "\"smem\": %zu, \"points\": %lld, \"bind_cap\": %d, \"any_dist\": %s, "
                  "\"bindings\": %s, \"grabs\": %s, \"contacts\": %s, \"self_collision\": %s, "
-                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld, \"warp_per_rod\": %s, \"one_warp_rod\": %s}",
+                 "\"sync_per_iteration\": %d, \"sync_per_step\": %lld, \"warp_per_rod\": %s, \"one_warp_rod\": %s, "
+                 "\"halo\": %s}",
                  i ? ", " : "", names[g.tier], g.variant, v.S, v.CAP, g.uni == 2 ? "\"launch\"" : (g.uni ? "true" : "false"), g.ncta,
                  g.grid, g.threads, g.cluster, g.smem, (long long)pts, g.bind_cap, g.any_dist ? "true" : "false",
                  binds ? "true" : "false", grabs ? "true" : "false", h->contacts_on ? "true" : "false",
-                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync, bwj, g.rw ? (g.rw_form == 1 ? "\"point_per_lane\"" : "\"two_per_lane\"") : "false");
+                 h->d.has_self ? "true" : "false", per_it, (long long)n_sync, bwj, g.rw ? (g.rw_form == 1 ? "\"point_per_lane\"" : "\"two_per_lane\"") : "false",
+                 (g.halo && h->halo_on) ? hj : "null");
         s += tmp;
     }
     s += std::string("], \"live\": ") + (h->live ? "true" : "false") + "}";

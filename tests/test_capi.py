@@ -195,3 +195,23 @@ def test_plan_barriers_per_step():
     assert plan(wl.insertion())[0]["sync_per_step"] == 33       # + contact phase
     assert plan(wl.knot())[0]["sync_per_step"] == 3 + 15 * 3    # + self-collision pairs
     assert plan(wl.hair(2048))[0]["sync_per_step"] == 23
+
+
+def test_plan_wide_halo_kernel():
+    # rod_halo.cuh: rods beyond one CTA (and one-CTA rods of >= 100 points)
+    # step with one inter-CTA exchange per step; cluster up to 16 CTAs of <=
+    # 256 threads, a co-resident grid beyond; the cfg1 cantilever, forced
+    # layouts and overlapping couplings keep the general kernel
+    def halo(w, **kw):
+        return plan(w, **kw)[0]["halo"]
+    h = halo(wl.pair())
+    assert h == {"ctas": 16, "threads": 160, "ghost": 21, "rods": 2, "bindings": True, "exchange": "cluster"}
+    assert halo(wl.extensible())["ghost"] == 1          # no colour sweeps: radius 1
+    assert halo(wl.sweep(16384))["exchange"] == "grid"
+    assert halo(wl.sweep(256))["exchange"] == "cluster"
+    assert halo(wl.cantilever()) is None
+    assert halo(wl.sweep(1024), force_tier=1, force_ctas=4) is None
+    assert halo(wl.hair(2048)) is None
+    w = wl.pair()
+    w.add_bindings(0, 1, 0, stride=5)
+    assert halo(w) is None

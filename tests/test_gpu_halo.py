@@ -1,0 +1,193 @@
+"""Wide-halo kernel (csrc/rod_halo.cuh): rods spread over a cluster (or a
+co-resident grid) with one inter-CTA exchange per step, bitwise against the
+oracle (oracle/rod_oracle.c, pinned to the reference core).
+
+Covers the cluster sizes and the grid exchange, one-way and bidirectional
+column bindings, drivers changed between epochs, extensible rods with
+external forces, one-CTA rods spread over a cluster, the exact redo when the
+speculative launch fails (tiny dividends), error stamps, iteration counts the
+ghost width no longer covers, grabs (general kernel), K = 1 launches and the
+tolerance modes.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2509_04277_b200 import state as st
+from paper_2509_04277_b200 import workloads as wl
+from paper_2509_04277_b200.engine import Engine
+from paper_2509_04277_b200.world import BIND_BIDIRECTIONAL, BIND_ONE_WAY
+
+from oracle.oracle import OracleStepper
+from test_gpu_parity import _tiny_world, assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+
+def halo_run(make, steps, k, env=None, monkeypatch=None, **kw):
+    """Step on the GPU and with the oracle; returns (gpu world, plan)."""
+    for key, v in (env or {}).items():
+        monkeypatch.setenv(key, str(v))
+    g, r = make(), make()
+    with Engine(g, **kw) as eng:
+        done = 0
+        while done < steps:
+            n = min(k, steps - done)
+            eng.run_epoch(n)
+            done += n
+        plan = eng.plan()
+        redo = eng.device_world.last_redo_count()
+    OracleStepper(r).run(steps)
+    assert_bitwise(g, r)
+    return g, plan["groups"][0], redo
+
+
+@pytest.mark.parametrize("ctas", [2, 5, 9, 16])
+def test_pair_cluster_sizes_bitwise(ctas, monkeypatch):
+    _, grp, redo = halo_run(wl.pair, 300, 10, {"RSB_HALO_CTAS": ctas}, monkeypatch)
+    assert grp["halo"]["ctas"] == ctas and grp["halo"]["bindings"] and grp["halo"]["rods"] == 2
+    assert grp["halo"]["exchange"] == "cluster"
+    assert redo == 0
+
+
+@pytest.mark.parametrize("make,k", [(wl.pair, 10), (lambda: wl.sweep(2048), 25),
+                                    (lambda: wl.extensible(512, 1.0), 10)])
+def test_grid_exchange_bitwise(make, k, monkeypatch):
+    _, grp, redo = halo_run(make, 200, k, {"RSB_HALO_GRID": 1}, monkeypatch)
+    assert grp["halo"]["exchange"] == "grid" and grp["halo"]["ctas"] > 1
+    assert redo == 0
+
+
+def test_long_rod_grid_exchange_default_bitwise():
+    # beyond a 16-CTA cluster the planner takes the grid exchange
+    _, grp, redo = halo_run(lambda: wl.sweep(16384), 30, 10)
+    assert grp["halo"]["exchange"] == "grid" and grp["halo"]["ctas"] > 16
+    assert redo == 0
+
+
+def _pair_custom(mode, stride):
+    def make():
+        w = wl._world()
+        for y in (1.5e-3, -1.5e-3):
+            w.add_rod(st.init_rod(201, 0.4, axis=(0.0, 0.0, 1.0), origin=(0.0, y, -0.4)),
+                      st.RodParams(**wl.MATERIAL))
+        w.finalize()
+        w.add_bindings(0, 1, mode, stride=stride)
+        w.set_driver(0)
+        w.driver_velocity[0] = (0.0, 0.01, 0.05)
+        return w
+    return make
+
+
+@pytest.mark.parametrize("mode,stride", [(BIND_ONE_WAY, 3), (BIND_BIDIRECTIONAL, 7), (BIND_ONE_WAY, 1)])
+def test_column_bindings_bitwise(mode, stride):
+    _, grp, _ = halo_run(_pair_custom(mode, stride), 200, 20)
+    assert grp["halo"] and grp["halo"]["bindings"]
+
+
+def test_overlapping_couplings_keep_the_general_kernel():
+    def make():
+        w = _pair_custom(BIND_BIDIRECTIONAL, 1)()
+        w.add_bindings(0, 1, BIND_ONE_WAY, stride=5)   # not a matching: sequential order
+        return w
+    _, grp, _ = halo_run(make, 60, 20)
+    assert grp["halo"] is None
+
+
+def test_driver_commands_between_epochs_bitwise():
+    def script(world, run):
+        run(30)
+        world.driver_velocity[0] = (0.01, 0.0, 0.08)
+        world.driver_velocity[1] = (0.0, -0.02, 0.0)
+        run(30)
+        world.driver_rotation[1] = 2.0
+        run(20)
+
+    g, r = wl.pair(), wl.pair()
+    with Engine(g) as eng:
+        assert eng.plan()["groups"][0]["halo"]
+        script(g, eng.run_epoch)
+    script(r, OracleStepper(r).run)
+    assert_bitwise(g, r)
+
+
+def test_extensible_with_external_forces_bitwise():
+    def make():
+        w = wl.extensible(700, 1.2)
+        w.external_forces[::7] = (1e-4, -2e-4, 5e-5)
+        return w
+    _, grp, redo = halo_run(make, 100, 10)
+    assert grp["halo"] and redo == 0
+
+
+@pytest.mark.parametrize("n", [128, 300, 512])
+def test_one_cta_rods_spread_over_a_cluster_bitwise(n):
+    _, grp, redo = halo_run(lambda: wl.sweep(n), 200, 50)
+    assert grp["tier"] == "cta" and grp["halo"] and grp["halo"]["ctas"] > 1
+    assert redo == 0
+
+
+def test_k1_launches_bitwise():
+    halo_run(wl.pair, 40, 1)
+    halo_run(lambda: wl.sweep(4096), 12, 1)
+
+
+def test_failed_speculation_redoes_exactly():
+    # velocities ~1e-200 on exactly representable geometry: colour-phase
+    # dividends below the fast path's window -- the cluster votes, nothing is
+    # written back and the exact general kernel steps the rod again
+    g, grp, redo = halo_run(lambda: _tiny_world(1, 700), 30, 10)
+    assert grp["halo"] and redo == 1
+    assert np.max(np.abs(g.velocities)) < 1e-150
+
+
+def test_planar_noise_takes_the_inline_fallback_not_the_redo():
+    # a planar cantilever's out-of-plane components decay through the
+    # subnormal range: those quotients go to the IEEE division in-kernel
+    g, _, redo = halo_run(lambda: wl.sweep(1024), 400, 100)
+    assert redo == 0
+
+
+def test_error_step_surfaces():
+    w = wl.sweep(1024)
+    with Engine(w) as eng:
+        assert eng.plan()["groups"][0]["halo"]
+        eng.run_epoch(5)
+        w.positions[300] = np.nan
+        with pytest.raises(FloatingPointError, match="non-finite"):
+            eng.run_epoch(5)
+
+
+def test_more_iterations_than_the_ghost_width_bitwise():
+    # the ghost width covers the planned iteration count; more iterations
+    # run on the general kernel, fewer stay on the halo kernel
+    g, r = wl.pair(), wl.pair()
+    ref = OracleStepper(r)
+    with Engine(g) as eng:
+        for it, steps in ((10, 30), (14, 30), (6, 30)):
+            eng.set_params(iterations=it)
+            ref.set_params(iterations=it)
+            eng.run_epoch(steps)
+            ref.run(steps)
+    assert_bitwise(g, r)
+
+
+def test_grab_falls_back_to_the_general_kernel_bitwise():
+    def make():
+        w = wl.sweep(1024)
+        w.grab(0, 700, (1.5, 0.05, 0.0))
+        return w
+    halo_run(make, 60, 20)
+
+
+def test_tolerance_modes():
+    # fp32 / fast fp64 through the halo kernel: within the stated bounds
+    for prec, tol_r in (("f32", 1e-5), ("f64_fast", 1e-9)):
+        g, r = wl.sweep(1024), wl.sweep(1024)
+        with Engine(g, precision=prec) as eng:
+            assert eng.plan()["groups"][0]["halo"]
+            eng.run_epoch(1000)
+        OracleStepper(r).run(1000)
+        L = 2e-3 * 1024
+        assert np.max(np.abs(g.positions - r.positions)) <= tol_r * L
+        assert np.max(np.abs(g.frames - r.frames)) <= (1e-4 if prec == "f32" else 1e-9)

@@ -1,0 +1,2 @@
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/r02be_pytest_gpu.log 2>&1; echo pytest=$?
+tail -15 gpurun_out/r02be_pytest_gpu.log
