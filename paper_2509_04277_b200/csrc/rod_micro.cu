@@ -179,7 +179,10 @@ __global__ void nb_sync_kernel(double* out, int iters) {
 // grid exchange, rod_halo.cuh): per round every CTA writes a halo word,
 // bar.sync, thread 0 fences, publishes its flag (release.gpu) and acquires
 // both neighbours', bar.sync, then reads the neighbour's word through L2.
-__global__ void grid_flag_kernel(double* out, int* flags, double* halo, int iters) {
+// mode 0: __threadfence + st.release + ld.acquire polls (the kernel's);
+//      1: st.release + ld.acquire, no fence (release cumulativity over the
+//         CTA barrier); 2: no fence, relaxed polls + one fence.acq_rel after
+__global__ void grid_flag_kernel(double* out, int* flags, double* halo, int iters, int mode) {
     const int rank = blockIdx.x, n = gridDim.x;
     const bool has_l = rank > 0, has_r = rank + 1 < n;
     double acc = 0;
@@ -190,15 +193,24 @@ __global__ void grid_flag_kernel(double* out, int* flags, double* halo, int iter
         if (threadIdx.x == 0) halo[2 * rank + (it & 1) * 2 * n] = double(it);
         __syncthreads();
         if (threadIdx.x == 0) {
-            __threadfence();
+            if (mode == 0) __threadfence();
             asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flags + rank), "r"(it + 1) : "memory");
             int v;
-            if (has_l)
-                do asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + rank - 1) : "memory");
-                while (v < it + 1);
-            if (has_r)
-                do asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + rank + 1) : "memory");
-                while (v < it + 1);
+            if (mode < 2) {
+                if (has_l)
+                    do asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + rank - 1) : "memory");
+                    while (v < it + 1);
+                if (has_r)
+                    do asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + rank + 1) : "memory");
+                    while (v < it + 1);
+            } else {
+                int vl = it + 1, vr = it + 1;
+                do {
+                    if (has_l) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(vl) : "l"(flags + rank - 1) : "memory");
+                    if (has_r) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(vr) : "l"(flags + rank + 1) : "memory");
+                } while (vl < it + 1 || vr < it + 1);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0 && has_r) acc += __ldcg(halo + 2 * (rank + 1) + (it & 1) * 2 * n);
@@ -286,13 +298,14 @@ cudaError_t run(int kind, int param, double* res) {
             case 12: {   // grid neighbour exchange, param CTAs (co-resident)
                 int* flags = nullptr;
                 double* halo = nullptr;
-                cudaError_t e2 = cudaMalloc(&flags, sizeof(int) * param);
-                if (e2 == cudaSuccess) e2 = cudaMalloc(&halo, sizeof(double) * 4 * param);
-                if (e2 == cudaSuccess) e2 = cudaMemset(flags, 0, sizeof(int) * param);
+                const int np_ = param & 0xffff;
+                cudaError_t e2 = cudaMalloc(&flags, sizeof(int) * np_);
+                if (e2 == cudaSuccess) e2 = cudaMalloc(&halo, sizeof(double) * 4 * np_);
+                if (e2 == cudaSuccess) e2 = cudaMemset(flags, 0, sizeof(int) * np_);
                 if (e2 == cudaSuccess) {
-                    int it = iters;
-                    void* args[] = {&buf, &flags, &halo, &it};
-                    e2 = cudaLaunchCooperativeKernel((const void*)grid_flag_kernel, dim3(param), dim3(128), args, 0, nullptr);
+                    int it = iters, mode = param >> 16, n = param & 0xffff;
+                    void* args[] = {&buf, &flags, &halo, &it, &mode};
+                    e2 = cudaLaunchCooperativeKernel((const void*)grid_flag_kernel, dim3(n), dim3(128), args, 0, nullptr);
                 }
                 if (e2 == cudaSuccess) e2 = cudaDeviceSynchronize();
                 cudaFree(flags);

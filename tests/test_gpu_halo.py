@@ -42,7 +42,7 @@ def halo_run(make, steps, k, env=None, monkeypatch=None, **kw):
     return g, plan["groups"][0], redo
 
 
-@pytest.mark.parametrize("ctas", [2, 5, 9, 16])
+@pytest.mark.parametrize("ctas", [4, 7, 12, 16])
 def test_pair_cluster_sizes_bitwise(ctas, monkeypatch):
     _, grp, redo = halo_run(wl.pair, 300, 10, {"RSB_HALO_CTAS": ctas}, monkeypatch)
     assert grp["halo"]["ctas"] == ctas and grp["halo"]["bindings"] and grp["halo"]["rods"] == 2
