@@ -191,7 +191,7 @@ struct StepArgs {
     // per rod W and ghost width G
     const HaloTask* htask;
     const int32_t *hdrv, *hbind;
-    int32_t h_nr, h_np, h_w, h_g;
+    int32_t h_nr, h_np, h_w, h_g, h_s;   // (h_s: steps per ghost exchange)
     int32_t h_poff[2], h_eoff[2];
 };
 

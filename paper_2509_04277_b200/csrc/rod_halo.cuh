@@ -27,10 +27,15 @@
 // through a ping-pong velocity buffer.  Bindings are done the same way by
 // the two threads of a bound column.
 //
-// Shared memory: the per-thread state fields are double-buffered by step
-// parity -- the owned boundary points of step s are pushed into the
-// neighbours' buffer (s+1)&1 while a slower neighbour may still read buffer
-// s&1 of step s (the cluster barrier of step s orders the reuse).
+// Exchange periods: with S steps per exchange the ghost width is S (2I+1)
+// (the grid exchange, an L2 round trip of 1-4 us, is amortised over S
+// steps; the ghosts step along redundantly in between).
+//
+// Shared memory: the per-thread state fields are double-buffered by
+// exchange-period parity -- the owned boundary points at the end of period p
+// are pushed into the neighbours' buffer (p+1)&1 while a slower neighbour may
+// still read buffer p&1 (the cluster barrier ending period p orders the
+// reuse).
 //
 // Quotients outside the fast path's window take the IEEE division inline
 // (one warp-uniform test per group of quotients); dividends below 2^-400 --
@@ -147,12 +152,16 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     // phase matters while its distance outside [o0, o1) is within the
     // dependency radius still to come (the outer ghost shell computes garbage
     // from missing neighbours and must neither fail the vote nor take the
-    // IEEE fallback).  Rg: radius after the gather (2I with colour sweeps).
+    // IEEE fallback).  The ghosts are exchanged every S = A.h_s steps; a
+    // step's radius is R1 = 2I + 1 with colour sweeps (scatter 1, gather 1,
+    // one per colour phase), 1 without; B: the radius still to come in the
+    // exchange period at the start of a step.
     const int d_l = tk.o0 - i, d_r = i - (tk.o1 - 1);
     const int dout = max(max(d_l, d_r), 0);
-    const int Rg = A.h_g - 1;
-    const bool m_sc = pv && d_l <= Rg + 1 && d_r <= Rg;   // scatter of element i
-    const bool m_ga = pv && dout <= Rg;                   // gather of point / frame i
+    const int S = A.h_s;
+    const bool sweeps = BIND || A.any_dist;
+    const int R1 = sweeps ? 2 * A.iters + 1 : 1;
+    const bool m_ga0 = pv && dout <= S * R1 - 1;   // statics used by the first step's sweeps
 
     // neighbours' thread index of a pushed point (same W everywhere)
     const bool has_l = rank > 0, has_r = rank + 1 < ncl;
@@ -192,13 +201,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const Real ws = im + im_up;
     const Real rws = rcp_rn(ws);
     const bool act = ev && dist && !(ws <= Real(0));
-    ok = ok & !(m_ga & act & !in_window(ws));
+    ok = ok & !(m_ga0 & act & !in_window(ws));
     const bool hl = pv && i > 0;   // element i-1 exists
     const uint32_t fl_l = hl ? A.pflags[pt - 1] : 0u;
     const Real ws_l = (hl ? A.invm[pt - 1] : Real(0)) + im;
     const Real rws_l = rcp_rn(ws_l);
     const bool act_l = hl && (fl_l & SF_DIST) && !(ws_l <= Real(0));
-    ok = ok & !(m_ga & act_l & !in_window(ws_l));
+    ok = ok & !(m_ga0 & act_l & !in_window(ws_l));
     // colour c: the element of colour c containing point i -- its own
     // (lower end) when i % 2 == c, the left one (upper end) otherwise
     const bool a_side[2] = {(i & 1) == 0, (i & 1) == 1};
@@ -235,10 +244,16 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     }
     const bool b_upd = bnd && (!b_is_a || bw_own > Real(0));   // one-way: a is never moved
 
-    int cur = 0;   // state buffer of this step
+    int cur = 0;   // state buffer of this exchange period
+    int jp = 0;    // step within the period
+    int nx = 0;    // exchanges so far
     for (int step = 0; step < A.steps; ++step) {
         const int sb = cur * HL_NSTATE;
-        if (!GX && step > 0 && !own) {   // ghosts: the state the neighbours pushed
+        const int B = (S - jp) * R1;
+        const bool m_sc = pv && d_l <= B && d_r <= B - 1;   // scatter of element i
+        const bool m_ga = pv && dout <= B - 1;              // gather of point / frame i
+        const bool m_in = pv && dout <= B - R1;             // integrate (feeds the next step)
+        if (!GX && step > 0 && jp == 0 && !own) {   // ghosts: the state the neighbours pushed
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 p[k] = HS(sb + HL_P + k, t);
@@ -248,7 +263,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
 #pragma unroll
             for (int k = 0; k < 4; ++k) q[k] = HS(sb + HL_Q + k, t);
         }
-        if (step == 0 || GX) {
+        if (step == 0 || GX || jp > 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 HS(sb + HL_P + k, t) = p[k];
@@ -310,7 +325,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             }
             const Real bdd = bd[0] * bd[0] + bd[1] * bd[1] + bd[2] * bd[2];
             bact = bnd && !(bdd == Real(0)) && !(bws == Real(0));
-            const bool bneed = bact && dout <= Rg - 2;   // the first binding phase's cone
+            const bool bneed = bact && dout <= B - 3;   // the first binding phase's cone
             bdist = sqrt_rn(bdd);
             const Real rbd = rcp_rn(bdist);
             const bool bdd_ok = in_window(bdd);
@@ -527,7 +542,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
             __syncthreads();
         }
-        int rem = Rg;   // radius still to come after the current phase
+        int rem = B - 1;   // radius still to come after the current phase
         for (int it = iters; it > 0; --it) {
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -581,18 +596,21 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             for (int k = 0; k < 4; ++k) qq4[k] = q[k] + h * dq[k];
             const Real qq = qq4[0] * qq4[0] + qq4[1] * qq4[1] + qq4[2] * qq4[2] + qq4[3] * qq4[3];
             const bool qq_ok = in_window(qq);
-            ok = ok & (!(own & ev) | qq_ok);
+            ok = ok & (!(m_in & ev) | qq_ok);
             const Real nrm = sqrt_rn(qq);
             const Real rn = rcp_rn(nrm);
             Real qn[4];
-            hl_div<4>(qq4, nrm, rn, qq_ok, own & ev, qn);
+            hl_div<4>(qq4, nrm, rn, qq_ok, m_in & ev, qn);
 #pragma unroll
             for (int k = 0; k < 4; ++k) q[k] = qn[k];
         }
 
-        // ===== exchange: owned state into this CTA's and the neighbours' next buffer =====
-        if (GX && step + 1 < A.steps) {
-            const int par = step & 1;
+        // ===== exchange (every S steps): owned boundary state to the neighbours =====
+        const bool xs = jp == S - 1 && step + 1 < A.steps;
+        jp = xs ? 0 : jp + 1;
+        if (GX && xs) {
+            const int par = nx & 1;
+            ++nx;
             Real* mine = A.halo + (size_t(par) * ncl + rank) * 2 * hrec;
             auto gput = [&](Real* b, int idx) {
                 Real* x = b + (size_t(r) * G + idx) * HL_NSTATE;
@@ -610,11 +628,11 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             __syncthreads();
             if (t == 0) {
                 __threadfence();
-                st_release_gpu(A.flags + rank, step + 1);
+                st_release_gpu(A.flags + rank, nx);
                 if (has_l)
-                    while (ld_acquire_gpu(A.flags + rank - 1) < step + 1) {}
+                    while (ld_acquire_gpu(A.flags + rank - 1) < nx) {}
                 if (has_r)
-                    while (ld_acquire_gpu(A.flags + rank + 1) < step + 1) {}
+                    while (ld_acquire_gpu(A.flags + rank + 1) < nx) {}
             }
             __syncthreads();
             if (pv && !own) {
@@ -632,8 +650,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) q[k] = ld_halo(x + HL_Q + k);
             }
-            cur ^= 1;
-        } else if (!GX && step + 1 < A.steps) {
+        } else if (!GX && xs) {
             cur ^= 1;
             const int nb = cur * HL_NSTATE;
             auto put = [&](Real* base, int x) {

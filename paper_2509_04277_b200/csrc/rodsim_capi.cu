@@ -147,6 +147,7 @@ struct Group {       // one kernel launch
     bool halo = false;
     bool h_gen = false, h_bind = false;
     int h_cta = 0, h_threads = 0, h_tb = 256, h_w = 0, h_g = 0, h_nr = 0, h_np = 0, h_iters = 0;
+    int h_s = 1;                    // steps per ghost exchange (ghost width h_s (2I+1))
     int32_t h_poff[2] = {0, 0}, h_eoff[2] = {0, 0};
     bool h_gx = false;              // grid exchange (co-resident grid) instead of one cluster
     std::vector<HaloTask> h_tasks;
@@ -162,6 +163,7 @@ struct Group {       // one kernel launch
 // a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
 constexpr int kSpecMinSteps = 32;
 constexpr int kHaloCtaMinPoints = 100;
+constexpr int kHaloGridSteps = 3;
 constexpr int kSpecBackoff = 64;
 bool spec_group(const Group& g) {
     return (g.tier == TIER_STREAM && g.variant == 7) || (g.tier == TIER_CTA && g.variant == 0);
@@ -199,6 +201,7 @@ struct rs_handle_s {
     int halo_ctas = 0;              // its CTA count (RSB_HALO_CTAS; 0: the planner's)
     int halo_grid = -1;             // RSB_HALO_GRID: 1 grid exchange, 0 cluster only, -1 the planner's
     int halo_width = 128;           // RSB_HALO_W: target threads per CTA of the grid exchange
+    int halo_steps = 0;             // RSB_HALO_STEPS: steps per exchange (0: the planner's)
     int halo_cta = -1;              // RSB_HALO_CTA: one-CTA segments (-1: from kHaloCtaMinPoints)
     int bw_shape = -1;              // its launch shape (RSB_BW_SHAPE, kBwShapes; -1: the planner's)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
@@ -543,13 +546,20 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
         // ghost width: the step's dependency radius (scatter 1, gather 1,
         // one per colour phase; without distance-projected elements or
         // bindings there are no sweeps)
-        const int G = (g.any_dist || bind) ? int(2 * d.iters + 1) : 1;
+        const int R1 = (g.any_dist || bind) ? int(2 * d.iters + 1) : 1;
         // one cluster of up to 16 CTAs while its CTAs stay within 256
         // threads (no spills); beyond, or on request, a co-resident grid of
         // CTAs of ~halo_width threads (more, thinner CTAs: a phase's issue
         // per SM is what bounds its latency)
         const int m_cl = int((np + kMaxCluster - 1) / kMaxCluster);
-        bool gx = h->halo_grid == 1 || (h->halo_grid != 0 && nr * (m_cl + 2 * G) > 256);
+        bool gx = h->halo_grid == 1 || (h->halo_grid != 0 && nr * (m_cl + 2 * R1) > 256);
+        // steps per exchange: the grid's exchange (an L2 round trip, 1-4 us)
+        // is amortised over kHaloGridSteps steps (cfg4 N = 16384, S = 1 / 2 / 3:
+        // 11.1 / 8.5 / 7.3 us per step; N = 8192: 9.8 / 7.5 / 7.1); a cluster
+        // barrier is worth wider ghosts only when they are one point per step
+        // (no colour sweeps: cfg2 3.80 -> 3.67 us at S = 2)
+        const int S = h->halo_steps > 0 ? h->halo_steps : (gx ? kHaloGridSteps : (R1 == 1 ? 2 : 1));
+        const int G = S * R1;
         int C;
         if (!gx) {
             C = h->halo_ctas > 0 ? h->halo_ctas : kMaxCluster;
@@ -597,6 +607,7 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
         g.h_threads = threads;
         g.h_tb = threads > 256 ? 512 : 256;
         g.h_g = G;
+        g.h_s = S;
         g.h_iters = int(d.iters);
         g.h_nr = nr;
         g.h_np = int(np);
@@ -1564,6 +1575,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.h_np = g.h_np;
     a.h_w = g.h_w;
     a.h_g = g.h_g;
+    a.h_s = g.h_s;
     for (int r = 0; r < 2; ++r) {
         a.h_poff[r] = g.h_poff[r];
         a.h_eoff[r] = g.h_eoff[r];
@@ -1714,7 +1726,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // exact general kernel follows in consume mode and runs only if the
     // halo launch's vote failed
     const bool halo = g.halo && h->halo_on && h->h_grabs.empty() && !h->live && cfg0 < 3 &&
-                      (g.h_g == 1 || 2 * h->d.iters + 1 <= g.h_g) &&
+                      (g.h_g == g.h_s || g.h_s * (2 * h->d.iters + 1) <= g.h_g) &&
                       h->redo_count.p && t_cnt < 0;
     if (halo) {
         CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
@@ -1933,6 +1945,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     if (const char* e = getenv("RSB_HALO_CTAS")) h->halo_ctas = atoi(e);
     if (const char* e = getenv("RSB_HALO_GRID")) h->halo_grid = atoi(e);
     if (const char* e = getenv("RSB_HALO_W")) h->halo_width = std::max(64, atoi(e));
+    if (const char* e = getenv("RSB_HALO_STEPS")) h->halo_steps = std::max(0, atoi(e));
     if (const char* e = getenv("RSB_HALO_CTA")) h->halo_cta = atoi(e);
     if (const char* sp = getenv("RSB_BW")) h->bw_on = atoi(sp) != 0;
     if (const char* sp = getenv("RSB_RW")) h->rw_on = atoi(sp) != 0;
@@ -2391,8 +2404,8 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
         char hj[200] = "null";
         if (g.halo)
             snprintf(hj, sizeof hj, "{\"ctas\": %d, \"threads\": %d, \"ghost\": %d, \"rods\": %d, \"bindings\": %s, "
-                     "\"exchange\": \"%s\"}",
-                     g.h_cta, g.h_threads, g.h_g, g.h_nr, g.h_bind ? "true" : "false", g.h_gx ? "grid" : "cluster");
+                     "\"exchange\": \"%s\", \"steps_per_exchange\": %d}",
+                     g.h_cta, g.h_threads, g.h_g, g.h_nr, g.h_bind ? "true" : "false", g.h_gx ? "grid" : "cluster", g.h_s);
         char tmp[1200];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "

@@ -205,8 +205,10 @@ def test_plan_wide_halo_kernel():
     def halo(w, **kw):
         return plan(w, **kw)[0]["halo"]
     h = halo(wl.pair())
-    assert h == {"ctas": 16, "threads": 160, "ghost": 21, "rods": 2, "bindings": True, "exchange": "cluster"}
-    assert halo(wl.extensible())["ghost"] == 1          # no colour sweeps: radius 1
+    assert h == {"ctas": 16, "threads": 160, "ghost": 21, "rods": 2, "bindings": True, "exchange": "cluster",
+                 "steps_per_exchange": 1}
+    assert halo(wl.extensible())["ghost"] == 2          # no colour sweeps: radius 1, 2 steps
+    assert halo(wl.sweep(16384))["steps_per_exchange"] == 3
     assert halo(wl.sweep(16384))["exchange"] == "grid"
     assert halo(wl.sweep(256))["exchange"] == "cluster"
     assert halo(wl.cantilever()) is None

@@ -58,6 +58,18 @@ def test_grid_exchange_bitwise(make, k, monkeypatch):
     assert redo == 0
 
 
+@pytest.mark.parametrize("steps", [1, 2, 3, 4])
+@pytest.mark.parametrize("grid", [0, 1])
+def test_exchange_periods_bitwise(steps, grid, monkeypatch):
+    # S steps per ghost exchange (ghost width S (2I+1)); K = 7 epochs end
+    # inside a period
+    _, grp, redo = halo_run(lambda: wl.sweep(1500), 70, 7,
+                            {"RSB_HALO_STEPS": steps, "RSB_HALO_GRID": grid}, monkeypatch)
+    assert grp["halo"]["steps_per_exchange"] == steps
+    assert grp["halo"]["exchange"] == ("grid" if grid else "cluster")
+    assert redo == 0
+
+
 def test_long_rod_grid_exchange_default_bitwise():
     # beyond a 16-CTA cluster the planner takes the grid exchange
     _, grp, redo = halo_run(lambda: wl.sweep(16384), 30, 10)

@@ -72,9 +72,11 @@ CASES = {
     "sweep8192": (lambda: wl.sweep(8192), 100),
     "sweep16384": (lambda: wl.sweep(16384), 100),
 }
-VARIANTS = [{}, {"RSB_HALO_CTA": 1}, {"RSB_HALO_CTA": 1, "RSB_HALO_CTAS": 4}, {"RSB_HALO_CTA": 1, "RSB_HALO_CTAS": 8},
-            {"RSB_HALO_GRID": 0}, {"RSB_HALO_GRID": 1}, {"RSB_HALO_GRID": 1, "RSB_HALO_W": 96},
-            {"RSB_HALO_GRID": 1, "RSB_HALO_W": 192}, {"RSB_HALO_GRID": 1, "RSB_HALO_W": 256}]
+VARIANTS = [{}, {"RSB_HALO_GRID": 0}, {"RSB_HALO_GRID": 1, "RSB_HALO_STEPS": 1},
+            {"RSB_HALO_GRID": 1, "RSB_HALO_STEPS": 2}, {"RSB_HALO_GRID": 1, "RSB_HALO_STEPS": 3},
+            {"RSB_HALO_GRID": 1, "RSB_HALO_STEPS": 2, "RSB_HALO_W": 192},
+            {"RSB_HALO_GRID": 1, "RSB_HALO_STEPS": 2, "RSB_HALO_W": 256},
+            {"RSB_HALO_GRID": 0, "RSB_HALO_STEPS": 2}]
 
 if __name__ == "__main__":
     which = sys.argv[1:] or list(CASES)
@@ -83,12 +85,14 @@ if __name__ == "__main__":
         out = {"case": name}
         out["parity_halo"] = parity(make, 200, k, {"RSB_HALO": 1})
         out["parity_halo_grid"] = parity(make, 200, k, {"RSB_HALO": 1, "RSB_HALO_GRID": 1})
+        out["parity_halo_s3"] = parity(make, 200, 7, {"RSB_HALO": 1, "RSB_HALO_STEPS": 3})
         out["general"] = timed(make, k, 50, {"RSB_HALO": 0})[0]
         for env in VARIANTS:
             key = "halo" + "".join(f"_{a[9:].lower()}{b}" for a, b in env.items())
             try:
                 us, h, redo = timed(make, k, 50, dict({"RSB_HALO": 1}, **env))
-                out[key] = {"us": round(us, 3), "plan": h and {x: h[x] for x in ("ctas", "threads", "exchange")},
+                out[key] = {"us": round(us, 3),
+                            "plan": h and {x: h[x] for x in ("ctas", "threads", "exchange", "steps_per_exchange")},
                             "redo": redo}
             except Exception as exc:  # noqa: BLE001
                 out[key] = str(exc)[:120]
