@@ -193,6 +193,10 @@ struct StepArgs {
     const int32_t *hdrv, *hbind;
     int32_t h_nr, h_np, h_w, h_g, h_s;   // (h_s: steps per ghost exchange)
     int32_t h_poff[2], h_eoff[2];
+    // the group's lazy-redo word: 0, or 1 + the first step of a launch
+    // whose vote failed (later launches of the group then skip; the host
+    // replays the exact kernel from that step at its next synchronisation)
+    int64_t* hfail;
 };
 
 constexpr int PROF_SLOTS = 64;

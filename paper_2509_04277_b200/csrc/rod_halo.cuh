@@ -49,10 +49,11 @@
 // depends on (a ghost's result of a phase matters while its distance outside
 // the owned range is within the radius still to come; the outer ghost shell
 // computes garbage from missing neighbours).  At the end of the launch the
-// cluster votes; if anything failed, nothing is written back and the flag in
-// A.redo_count makes the exact general cluster kernel, launched right after
-// in consume mode, step the segment again from the launch-start state (it
-// exits at once otherwise).
+// cluster votes; if anything failed, nothing is written back and the launch's
+// first step goes into the group's redo word: later launches of the group
+// return at once, and the host, at its next synchronisation, replays the
+// exact general kernel from that step (results do not depend on how steps
+// are split into launches) -- no second launch per epoch in the common case.
 //
 // Arithmetic: the reference's expression order (oracle/rod_oracle.c cites
 // _core.pyx), identical to rod_warp1.cuh / rod_step.cuh.
@@ -124,6 +125,9 @@ template <typename Real, int MODE, bool GEN, bool BIND, int TB, bool GX>
 __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // an earlier launch of this group failed its vote: the host replays
+    // the exact kernel from that launch's first step, this one does nothing
+    if (*reinterpret_cast<volatile int64_t*>(A.hfail)) return;
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Real* sm = reinterpret_cast<Real*>(smem_raw);
@@ -148,6 +152,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const bool l_ok = in_window(A.u.l);
     const bool I_ok = in_window(A.u.I[0]) & in_window(A.u.I[1]) & in_window(A.u.I[2]);
     bool ok = true;
+    unsigned why = 0;   // RSB_DEBUG bit 2: which checks failed (rs_destroy prints the mask)
+#define OKC(bit, cond)                      \
+    do {                                    \
+        const bool c_ = (cond);             \
+        ok = ok & c_;                       \
+        if (A.debug & 4) why |= c_ ? 0u : unsigned(bit); \
+    } while (0)
     // Which results the owned range depends on: a thread's result of a
     // phase matters while its distance outside [o0, o1) is within the
     // dependency radius still to come (the outer ghost shell computes garbage
@@ -201,13 +212,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const Real ws = im + im_up;
     const Real rws = rcp_rn(ws);
     const bool act = ev && dist && !(ws <= Real(0));
-    ok = ok & !(m_ga0 & act & !in_window(ws));
+    OKC(1, !(m_ga0 & act & !in_window(ws)));
     const bool hl = pv && i > 0;   // element i-1 exists
     const uint32_t fl_l = hl ? A.pflags[pt - 1] : 0u;
     const Real ws_l = (hl ? A.invm[pt - 1] : Real(0)) + im;
     const Real rws_l = rcp_rn(ws_l);
     const bool act_l = hl && (fl_l & SF_DIST) && !(ws_l <= Real(0));
-    ok = ok & !(m_ga0 & act_l & !in_window(ws_l));
+    OKC(1, !(m_ga0 & act_l & !in_window(ws_l)));
     // colour c: the element of colour c containing point i -- its own
     // (lower end) when i % 2 == c, the left one (upper end) otherwise
     const bool a_side[2] = {(i & 1) == 0, (i & 1) == 1};
@@ -291,7 +302,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         const Real dd = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
         const bool sc = m_sc & ev;
         const bool dd_ok = in_window(dd);
-        ok = ok & (!sc | dd_ok);   // a degenerate segment: the exact kernel stamps it
+        OKC(2, (!sc | dd_ok));   // a degenerate segment: the exact kernel stamps it
         const Real len = sqrt_rn(dd);
         const Real rlen = rcp_rn(len);
         // the phase's quotients on the fast path; a lane that needs one
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             bdist = sqrt_rn(bdd);
             const Real rbd = rcp_rn(bdist);
             const bool bdd_ok = in_window(bdd);
-            ok = ok & (!bneed | (bdd_ok & in_window(bws)));
+            OKC(4, (!bneed | (bdd_ok & in_window(bws))));
 #pragma unroll
             for (int k = 0; k < 3; ++k) bnq[k] = fq(bd[k], bdist, rbd, bdd_ok, bneed);
             bbias = fq(beta * bdist, dt, rdt, dt_ok, bneed);
@@ -462,7 +473,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                 const Real g = f[k] - efl[k];
                 f[k] = hp ? g : f[k];
             }
-            ok = ok & (!m_ga | (isfinite(f[0]) & isfinite(f[1]) & isfinite(f[2])));
+            OKC(8, (!m_ga | (isfinite(f[0]) & isfinite(f[1]) & isfinite(f[2]))));
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 a_v[k] = dt * f[k];
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                 const Real g2 = tau[k] - jtl[k];
                 tau[k] = jp ? g2 : tau[k];
             }
-            ok = ok & (!(m_ga & ev) | (isfinite(tau[0]) & isfinite(tau[1]) & isfinite(tau[2])));
+            OKC(16, (!(m_ga & ev) | (isfinite(tau[0]) & isfinite(tau[1]) & isfinite(tau[2]))));
 #pragma unroll
             for (int k = 0; k < 3; ++k) iw[k] = A.u.I[k] * w[k];
             gy[0] = w[1] * iw[2] - w[2] * iw[1];
@@ -535,52 +546,85 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         }
         // (rods without distance-projected elements and bindings: no sweeps,
         // like the general kernel)
-        int vb_off = HL_VA;
+        // The sweeps run on the fast quotients; a lane whose result the
+        // owned range needs and whose dividend left the window (rare: tiny
+        // impulses early in a run) is noted, the notes ORed into the sweeps'
+        // last barrier, and then this CTA alone replays its sweeps from the
+        // post-gather velocities with the IEEE division for such lanes (one
+        // warp-uniform test per phase) -- its neighbours are unaffected.
         const int iters = (BIND || A.any_dist) ? A.iters : 0;
-        if (iters > 0) {
+        const Real v_g[3] = {v[0], v[1], v[2]};
+        auto sweeps = [&](auto careful_c) -> int {
+            constexpr bool CAREFUL = decltype(careful_c)::value;
+            int vb_off = HL_VA;
+            bool noted = false;
+            int any_noted = 0;
 #pragma unroll
             for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
             __syncthreads();
-        }
-        int rem = B - 1;   // radius still to come after the current phase
-        for (int it = iters; it > 0; --it) {
+            int rem = B - 1;   // radius still to come after the current phase
+            for (int it = iters; it > 0; --it) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                --rem;
-                const bool chk = pv && dout <= rem;
-                Real dv[3];
+                for (int c = 0; c < 2; ++c) {
+                    --rem;
+                    const bool chk = pv && dout <= rem;
+                    Real dv[3];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) dv[k] = HS(vb_off + k, partner[c]) - v[k];
-                Real x = dv[0] * nP[c][0];
-                x = x + dv[1] * nP[c][1];
-                x = x + dv[2] * nP[c][2];
-                x = x + bP[c];
-                const Real q0 = (-x) * rwsP[c];
-                Real lam = fma(fma(-q0, wsP[c], -x), rwsP[c], q0);
-                const bool z = is_zero(x);
-                if (z) lam = Real(-0.0);
-                ok = ok & !(chk & actP[c] & !(in_window(x) | z));
+                    for (int k = 0; k < 3; ++k) dv[k] = HS(vb_off + k, partner[c]) - v[k];
+                    Real x = dv[0] * nP[c][0];
+                    x = x + dv[1] * nP[c][1];
+                    x = x + dv[2] * nP[c][2];
+                    x = x + bP[c];
+                    const Real q0 = (-x) * rwsP[c];
+                    Real lam = fma(fma(-q0, wsP[c], -x), rwsP[c], q0);
+                    const bool z = is_zero(x);
+                    if (z) lam = Real(-0.0);
+                    const bool off = chk & actP[c] & !(in_window(x) | z);
+                    if constexpr (CAREFUL) {
+                        // the reference's -(((0 + p0) + p1) + p2 + bias) / w_sum
+                        if (__any_sync(0xffffffffu, off))
+                            if (off) lam = div_ieee(-(x + Real(0.0)), wsP[c]);
+                    } else {
+                        noted = noted | off;
+                        if (A.debug & 4) why |= off ? 32u : 0u;
+                    }
 #pragma unroll
-                for (int k = 0; k < 3; ++k) sub_if(actP[c], v[k], im * lam * nP[c][k]);
-                vb_off = HL_VA + HL_VB - vb_off;
+                    for (int k = 0; k < 3; ++k) sub_if(actP[c], v[k], im * lam * nP[c][k]);
+                    vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                __syncthreads();
+                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+                    if (!CAREFUL && it == 1 && c == 1 && !BIND) any_noted = __syncthreads_or(noted);
+                    else __syncthreads();
+                }
+                if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
+                    Real vrel = Real(0.0);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) vrel = vrel + (HS(vb_off + k, t_b) - v[k]) * bn[k];
+                    bool lok = true;
+                    Real lam = hl_quot(-(vrel + bbias), bws, brws, lok);
+                    const bool off = bact & (dout <= rem) & !lok;
+                    if constexpr (CAREFUL) {
+                        if (__any_sync(0xffffffffu, off))
+                            if (off) lam = div_ieee(-(vrel + bbias), bws);
+                    } else {
+                        noted = noted | off;
+                        if (A.debug & 4) why |= off ? 64u : 0u;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * lam * bn[k]);
+                    vb_off = HL_VA + HL_VB - vb_off;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+                    if (!CAREFUL && it == 1) any_noted = __syncthreads_or(noted);
+                    else __syncthreads();
+                }
             }
-            if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
-                Real vrel = Real(0.0);
+            return any_noted;
+        };
+        if (iters > 0 && sweeps(std::false_type{})) {
 #pragma unroll
-                for (int k = 0; k < 3; ++k) vrel = vrel + (HS(vb_off + k, t_b) - v[k]) * bn[k];
-                bool lok = true;
-                const Real lam = hl_quot(-(vrel + bbias), bws, brws, lok);
-                ok = ok & (!(bact & (dout <= rem)) | lok);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * lam * bn[k]);
-                vb_off = HL_VA + HL_VB - vb_off;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                __syncthreads();
-            }
+            for (int k = 0; k < 3; ++k) v[k] = v_g[k];
+            sweeps(std::true_type{});
         }
 
         // ================= integrate (_core.pyx:1023-1042) =================
@@ -596,7 +640,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             for (int k = 0; k < 4; ++k) qq4[k] = q[k] + h * dq[k];
             const Real qq = qq4[0] * qq4[0] + qq4[1] * qq4[1] + qq4[2] * qq4[2] + qq4[3] * qq4[3];
             const bool qq_ok = in_window(qq);
-            ok = ok & (!(m_in & ev) | qq_ok);
+            OKC(128, (!(m_in & ev) | qq_ok));
             const Real nrm = sqrt_rn(qq);
             const Real rn = rcp_rn(nrm);
             Real qn[4];
@@ -678,16 +722,15 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     if constexpr (GX) {
         // grid: OR into the redo word, then an arrival count over all CTAs
         // (co-resident) before anyone reads it
-        if (t == 0) {
-            if (bad) atomicOr(A.redo_count, 1);
+        if (t == 0) {   // flags[ncl]: arrivals, flags[ncl + 1]: the OR of the votes
+            if (bad) atomicOr(A.flags + ncl + 1, 1);
             __threadfence();
             atomicAdd(A.flags + ncl, 1);
             while (ld_acquire_gpu(A.flags + ncl) < int(ncl)) {}
-            *vote = ld_acquire_gpu(A.redo_count);
+            *vote = ld_acquire_gpu(A.flags + ncl + 1);
         }
         __syncthreads();
         any = *vote;
-        if (any) return;
     } else {
         if (t == 0) *vote = bad;
         cluster_barrier();
@@ -695,11 +738,10 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         any = __syncthreads_or(any);
         cluster_barrier();   // every remote read done before a CTA exits
     }
-    if (any) {   // (a one-CTA group's exact launch steps the listed task 0)
-        if (rank == 0 && t == 0) {
-            A.redo_list[0] = 0;
-            *A.redo_count = 1;
-        }
+    if ((A.debug & 4) && why && A.prof) atomicOr(A.prof + PROF_SLOTS - 1, (unsigned long long)why);
+#undef OKC
+    if (any) {   // nothing written back: the host replays this launch exactly
+        if (rank == 0 && t == 0) *A.hfail = A.step0 + 1;
         return;
     }
     if (own) {

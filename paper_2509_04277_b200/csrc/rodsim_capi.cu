@@ -152,7 +152,8 @@ struct Group {       // one kernel launch
     bool h_gx = false;              // grid exchange (co-resident grid) instead of one cluster
     std::vector<HaloTask> h_tasks;
     HaloTask* d_htask = nullptr;
-    int32_t* d_hflags = nullptr;    // grid exchange: per-CTA step flags + arrival count
+    int32_t* d_hflags = nullptr;    // grid exchange: per-CTA flags, arrival count, vote OR
+    int64_t* d_hfail = nullptr;     // lazy redo word (StepArgs::hfail)
     void* d_hhalo = nullptr;        // grid exchange: (2, C, 2, NR, G, 13) halo records
 };
 
@@ -202,6 +203,9 @@ struct rs_handle_s {
     int halo_grid = -1;             // RSB_HALO_GRID: 1 grid exchange, 0 cluster only, -1 the planner's
     int halo_width = 128;           // RSB_HALO_W: target threads per CTA of the grid exchange
     int halo_steps = 0;             // RSB_HALO_STEPS: steps per exchange (0: the planner's)
+    bool halo_pending = false;      // wide-halo launches not yet checked for a failed vote
+    bool last_halo = false;         // the last launch was a wide-halo launch
+    int64_t halo_redone = 0;        // groups replayed exactly at the last check
     int halo_cta = -1;              // RSB_HALO_CTA: one-CTA segments (-1: from kHaloCtaMinPoints)
     int bw_shape = -1;              // its launch shape (RSB_BW_SHAPE, kBwShapes; -1: the planner's)
     DevBuf redo_list, redo_count;   // rods the speculative launch left to the exact one
@@ -634,18 +638,15 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
         int rc = halo_query(h, g, &occ);
         if (rc) return rc;
         if (occ < 1 || (gx && int64_t(occ) * h->num_sms < C)) continue;
+        CK(cudaMalloc(&g.d_hfail, sizeof(int64_t)));
+        CK(cudaMemset(g.d_hfail, 0, sizeof(int64_t)));
         if (gx) {
-            CK(cudaMalloc(&g.d_hflags, sizeof(int32_t) * size_t(C + 1)));
+            CK(cudaMalloc(&g.d_hflags, sizeof(int32_t) * size_t(C + 2)));
             const size_t words = size_t(2) * C * 2 * nr * G * HL_NSTATE;
             CK(cudaMalloc(&g.d_hhalo, h->rsz * words));
         }
         CK(cudaMalloc(&g.d_htask, sizeof(HaloTask) * ts.size()));
         CK(cudaMemcpy(g.d_htask, ts.data(), sizeof(HaloTask) * ts.size(), cudaMemcpyHostToDevice));
-        if (!h->redo_count.p || !h->redo_list.p) {   // (a one-CTA group's exact launch reads the list)
-            int rc2 = dev_alloc(h->redo_count, sizeof(int32_t));
-            if (!rc2 && !h->redo_list.p) rc2 = dev_alloc(h->redo_list, sizeof(int32_t));
-            if (rc2) return rc2;
-        }
         g.halo = true;
     }
     return RS_OK;
@@ -772,6 +773,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         if (g.d_htask) cudaFree(g.d_htask);
         if (g.d_hflags) cudaFree(g.d_hflags);
         if (g.d_hhalo) cudaFree(g.d_hhalo);
+        if (g.d_hfail) cudaFree(g.d_hfail);
     }
     h->h_tasks.clear();
     h->h_binds.clear();
@@ -1576,6 +1578,7 @@ StepArgs<Real> make_args(rs_handle h, const Group& g, int64_t step0, int steps) 
     a.h_w = g.h_w;
     a.h_g = g.h_g;
     a.h_s = g.h_s;
+    a.hfail = g.d_hfail;
     for (int r = 0; r < 2; ++r) {
         a.h_poff[r] = g.h_poff[r];
         a.h_eoff[r] = g.h_eoff[r];
@@ -1602,7 +1605,8 @@ int halo_query(rs_handle h, const Group& g, int* out) {
 // Launch one group, or (t_cnt >= 0, CTA/stream tiers only) the task
 // sub-range [t_off, t_off + t_cnt) of it: tasks of those tiers are
 // independent, so a sub-range is a complete launch of its own.
-int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_off = 0, int t_cnt = -1) {
+int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_off = 0, int t_cnt = -1,
+                 bool exact = false) {
     if (g.tier == TIER_GRID) CK(cudaMemsetAsync(g.d_flags, 0, sizeof(int32_t) * g.ncta, h->st));
     const int nt = t_cnt < 0 ? g.ncta : t_cnt;
     const int grid = t_cnt < 0 ? g.grid : (g.tier == TIER_STREAM ? std::min(g.grid, nt) : nt);
@@ -1613,7 +1617,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // list and returns)
     // (one-CTA rods only for long epochs: the exact launch over the redo
     // list costs a few microseconds, a whole K = 1 step on a short rod)
-    bool spec = h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
+    bool spec = !exact && h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
                 (g.tier != TIER_CTA || steps >= kSpecMinSteps);
     const int gi = int(&g - h->groups.data());
     const bool backoff = g.tier == TIER_CTA && gi >= 0 && gi < int(h->groups.size());
@@ -1721,24 +1725,15 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         auto a = go(make_args<double>(h, g, step0, steps));
         return f64fast::warp_step<double>(gen, g.rw_form, &a, nt, h->st);
     };
-    // the wide-halo kernel takes the launch of an eligible cluster group
-    // (no grabs, not live, ghost width still covering the iterations); the
-    // exact general kernel follows in consume mode and runs only if the
-    // halo launch's vote failed
-    const bool halo = g.halo && h->halo_on && h->h_grabs.empty() && !h->live && cfg0 < 3 &&
-                      (g.h_g == g.h_s || g.h_s * (2 * h->d.iters + 1) <= g.h_g) &&
-                      h->redo_count.p && t_cnt < 0;
+    // the wide-halo kernel takes the launch of an eligible group (no grabs,
+    // not live, ghost width still covering the iterations); a failed vote is
+    // replayed exactly by resolve_halo at the next synchronisation
+    const bool halo = !exact && g.halo && h->halo_on && h->h_grabs.empty() && !h->live && cfg0 < 3 &&
+                      (g.h_g == g.h_s || g.h_s * (2 * h->d.iters + 1) <= g.h_g) && t_cnt < 0;
     if (halo) {
-        CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
-        if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 1), h->st));
+        if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 2), h->st));
         const int gen = (g.h_gen || h->has_fext) ? 1 : 0, bind = g.h_bind ? 1 : 0;
-        auto go = [&](auto a) {
-            a.redo_count = static_cast<int32_t*>(h->redo_count.p);
-            a.redo_list = static_cast<int32_t*>(h->redo_list.p);
-            a.redo_mode = 1;
-            return a;
-        };
-        // the halo launch's own exchange buffers (the general kernel keeps its own)
+        // the halo launch's own exchange buffers
         auto hx = [&](auto a) {
             a.flags = g.d_hflags;
             a.halo = static_cast<decltype(a.halo)>(g.d_hhalo);
@@ -1746,28 +1741,25 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         };
         cudaError_t eh;
         if (h->prec == RS_F64_MIRROR) {
-            auto a = go(make_args<double>(h, g, step0, steps));
-            auto ah = hx(a);
-            eh = mirror::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &ah, g.h_cta, g.h_threads, h->st, nullptr);
-            if (eh == cudaSuccess) eh = mirror::launch_step<double>(g.variant, g.tier, cfg0, a, grid, g.threads, g.smem, g.cluster, h->st);
+            auto a = hx(make_args<double>(h, g, step0, steps));
+            eh = mirror::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &a, g.h_cta, g.h_threads, h->st, nullptr);
         } else if (h->prec == RS_F32) {
-            auto a = go(make_args<float>(h, g, step0, steps));
-            auto ah = hx(a);
-            eh = f32::halo_step<float>(0, gen, bind, g.h_tb, g.h_gx, &ah, g.h_cta, g.h_threads, h->st, nullptr);
-            if (eh == cudaSuccess) eh = f32::launch_step<float>(g.variant, g.tier, cfg0, a, grid, g.threads, g.smem, g.cluster, h->st);
+            auto a = hx(make_args<float>(h, g, step0, steps));
+            eh = f32::halo_step<float>(0, gen, bind, g.h_tb, g.h_gx, &a, g.h_cta, g.h_threads, h->st, nullptr);
         } else {
-            auto a = go(make_args<double>(h, g, step0, steps));
-            auto ah = hx(a);
-            eh = f64fast::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &ah, g.h_cta, g.h_threads, h->st, nullptr);
-            if (eh == cudaSuccess) eh = f64fast::launch_step<double>(g.variant, g.tier, cfg0, a, grid, g.threads, g.smem, g.cluster, h->st);
+            auto a = hx(make_args<double>(h, g, step0, steps));
+            eh = f64fast::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &a, g.h_cta, g.h_threads, h->st, nullptr);
         }
         if (eh != cudaSuccess)
             return fail(RS_E_CUDA, "wide-halo launch (%d CTAs x %d threads) failed: %s", g.h_cta, g.h_threads,
                         cudaGetErrorString(eh));
-        h->last_spec = true;
-        h->launches += 2;
+        h->halo_pending = true;
+        h->last_halo = true;
+        h->last_spec = false;
+        h->launches += 1;
         return RS_OK;
     }
+    h->last_halo = false;
     cudaError_t e = bw ? one_bw() : rw ? one_rw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
     if (e == cudaSuccess && spec) e = one(cfg0, 1);
     if (e == cudaSuccess && spec && backoff && !h->redo_ev_live[gi]) {
@@ -1783,6 +1775,37 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     return RS_OK;
 }
 
+// Wide-halo launches whose cluster vote failed wrote nothing back and left
+// their first step in the group's redo word (later launches of the group
+// returned at once): replay the exact general kernel from that step to the
+// current one.  Called before anything reads or replaces the device state
+// or changes what a replay would compute (synchronisation, download, upload,
+// staged commands, parameters).
+int resolve_halo(rs_handle h) {
+    if (!h->halo_pending) return RS_OK;
+    h->halo_pending = false;
+    int64_t redone = 0;
+    for (const Group& g : h->groups) {
+        if (!g.d_hfail) continue;
+        int64_t v = 0;
+        CK(cudaMemcpyAsync(&v, g.d_hfail, sizeof v, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        if (!v) continue;
+        CK(cudaMemsetAsync(g.d_hfail, 0, sizeof(int64_t), h->st));
+        const bool lh = h->last_halo;
+        for (int64_t s0 = v - 1; s0 < h->step;) {
+            const int k = int(std::min<int64_t>(h->step - s0, kMaxStepsPerLaunch));
+            int rc = launch_group(h, g, s0, k, 0, -1, true);
+            if (rc) return rc;
+            s0 += k;
+        }
+        h->last_halo = lh;
+        ++redone;
+    }
+    h->halo_redone = redone;
+    return RS_OK;
+}
+
 void register_host(rs_handle h, void* p, size_t bytes) {
     if (!p || bytes == 0) return;   // page-locked: async copies, no staging
     if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess)
@@ -1795,6 +1818,11 @@ void register_host(rs_handle h, void* p, size_t bytes) {
 
 // ph_boundary at the epoch's first step: staged commands, dirty controls
 int epoch_prelude(rs_handle h) {
+    // (staged commands or new controls would reach a replay of earlier steps)
+    if (h->halo_pending && (h->control_dirty || (h->ring && h->ring->tail != h->ring->head))) {
+        int rc = resolve_halo(h);
+        if (rc) return rc;
+    }
     if (!h->live) drain_ring(h);   // live launches drain in the kernel
     if (h->control_dirty) {
         int rc = upload_control(h);
@@ -1999,7 +2027,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     *h->h_err = 0;
     if (cudaMemset(h->d_err, 0, sizeof(unsigned long long)) != cudaSuccess)
         return bail(fail(RS_E_CUDA, "memset failed"));
-    if ((h->debug & 2) && (cudaMalloc(&h->d_prof, PROF_SLOTS * sizeof(unsigned long long)) != cudaSuccess ||
+    if ((h->debug & 6) && (cudaMalloc(&h->d_prof, PROF_SLOTS * sizeof(unsigned long long)) != cudaSuccess ||
                            cudaMemset(h->d_prof, 0, PROF_SLOTS * sizeof(unsigned long long)) != cudaSuccess))
         return bail(fail(RS_E_CUDA, "profile buffer allocation failed"));
     if (h->rsz == sizeof(double)) {
@@ -2021,6 +2049,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
 int rs_upload(rs_handle h, uint32_t mask) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     CK(cudaSetDevice(h->d.device));
+    if (int rc = resolve_halo(h)) return rc;
     int rc = RS_OK;
     if (mask & RS_CONTROL) {
         if ((rc = upload_control(h))) return rc;
@@ -2062,6 +2091,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
 int rs_synchronize(rs_handle h) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     CK(cudaSetDevice(h->d.device));
+    if (int rc = resolve_halo(h)) return rc;
     if (h->err_pending) {
         CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
         h->err_pending = false;
@@ -2104,6 +2134,7 @@ int download_control(rs_handle h) {
 int rs_download(rs_handle h, uint32_t mask) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     CK(cudaSetDevice(h->d.device));
+    if (int rc = resolve_halo(h)) return rc;
     const rs_world_desc& d = h->d;
     int rc = RS_OK;
     if ((mask & (RS_STATE | RS_CONTROL)) && h->live && h->planned)
@@ -2151,6 +2182,7 @@ int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* ba
     if (!h) return fail(RS_E_INVALID, "null handle");
     if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
     CK(cudaSetDevice(h->d.device));
+    if (int rc = resolve_halo(h)) return rc;
     const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 && !h->contacts_on &&
                            !h->d.has_mesh && !h->d.has_self &&
                            (h->groups[0].tier == TIER_CTA || h->groups[0].tier == TIER_STREAM) &&
@@ -2177,6 +2209,10 @@ int64_t rs_step_counter(rs_handle h) { return h ? h->step : -1; }
 
 int rs_update_params(rs_handle h, double dt, int64_t iters) {
     if (!h) return fail(RS_E_INVALID, "null handle");
+    if (h->halo_pending) {   // a replay runs with the parameters of its steps
+        CK(cudaSetDevice(h->d.device));
+        if (int rc = resolve_halo(h)) return rc;
+    }
     if (dt <= 0.0 || iters < 1) return fail(RS_E_INVALID, "dt must be positive and iters >= 1");
     h->d.dt = dt;
     h->d.iters = iters;
@@ -2282,11 +2318,17 @@ void rs_destroy(rs_handle h) {
         if (g.d_htask) cudaFree(g.d_htask);
         if (g.d_hflags) cudaFree(g.d_hflags);
         if (g.d_hhalo) cudaFree(g.d_hhalo);
+        if (g.d_hfail) cudaFree(g.d_hfail);
     }
     for (void* p : h->registered) cudaHostUnregister(p);
     for (cudaEvent_t e : h->redo_ev)
         if (e) cudaEventDestroy(e);
     if (h->h_redo) cudaFreeHost(h->h_redo);
+    if (h->d_prof && (h->debug & 4)) {   // wide-halo failed checks (RSB_DEBUG bit 2)
+        unsigned long long v = 0;
+        if (cudaMemcpy(&v, h->d_prof + PROF_SLOTS - 1, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
+            fprintf(stderr, "rsb-halo-fail-mask 0x%llx\n", v);
+    }
     if (h->d_prof) {   // per-phase profile (RSB_DEBUG=2): cycles per step, CTA 0
         unsigned long long v[PROF_SLOTS];
         if (cudaMemcpy(v, h->d_prof, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess && h->prof_steps > 0) {
@@ -2340,6 +2382,10 @@ int64_t rs_launch_count(rs_handle h) { return h ? h->launches : -1; }
 
 int64_t rs_last_redo_count(rs_handle h) {
     if (!h) return -1;
+    if (h->last_halo) {   // wide-halo groups replayed exactly at the last check
+        if (cudaSetDevice(h->d.device) != cudaSuccess || resolve_halo(h) != RS_OK) return -1;
+        return h->halo_redone;
+    }
     if (!h->redo_count.p || !h->last_spec) return 0;   // the last launch did not speculate
     if (cudaSetDevice(h->d.device) != cudaSuccess) return -1;
     int32_t n = 0;
@@ -2447,6 +2493,10 @@ int rs_plan_dry(const rs_world_desc* desc, int32_t num_sms, char* buf, int64_t l
 
 int rs_device_ptr(rs_handle h, int32_t which, void** out) {
     if (!h || !out) return fail(RS_E_INVALID, "null argument");
+    if (h->halo_pending) {   // the buffers must hold every launched step
+        CK(cudaSetDevice(h->d.device));
+        if (int rc = resolve_halo(h)) return rc;
+    }
     const DevBuf* b[] = {&h->pos, &h->vel, &h->q, &h->w};
     if (which < 0 || which > 3) return fail(RS_E_INVALID, "unknown array");
     *out = b[which]->p;

@@ -144,13 +144,37 @@ def test_k1_launches_bitwise():
     halo_run(lambda: wl.sweep(4096), 12, 1)
 
 
-def test_failed_speculation_redoes_exactly():
+def test_tiny_dividends_replay_the_sweeps_in_the_cta():
     # velocities ~1e-200 on exactly representable geometry: colour-phase
-    # dividends below the fast path's window -- the cluster votes, nothing is
-    # written back and the exact general kernel steps the rod again
+    # dividends below the fast path's window -- the CTA replays its sweeps
+    # with IEEE divisions for those lanes, no launch fails its vote
     g, grp, redo = halo_run(lambda: _tiny_world(1, 700), 30, 10)
-    assert grp["halo"] and redo == 1
+    assert grp["halo"] and redo == 0
     assert np.max(np.abs(g.velocities)) < 1e-150
+
+
+def _degenerate_sweep():
+    w = wl.sweep(1024)
+    w.positions[501] = w.positions[500]   # a zero-length segment at step 0
+    return w
+
+
+def test_failed_vote_replays_the_skipped_launches():
+    # a degenerate segment (the reference stamps its error step): the first
+    # device-resident launch fails its vote, the later ones return at once,
+    # and the download replays all 26 steps on the exact kernel
+    from paper_2509_04277_b200 import _lib
+    g, r = _degenerate_sweep(), _degenerate_sweep()
+    with Engine(g) as eng:
+        dev = eng.device_world
+        for _ in range(3):
+            dev.run(7)
+        assert dev.last_redo_count() == 1
+        dev.run(5)
+        dev.download(_lib.RS_STATE)
+        assert dev.error_step() == 0
+    OracleStepper(r).run(26)
+    assert_bitwise(g, r)
 
 
 def test_planar_noise_takes_the_inline_fallback_not_the_redo():
