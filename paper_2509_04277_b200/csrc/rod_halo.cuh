@@ -254,6 +254,14 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         bw_own = b_is_a ? wa : wb;
     }
     const bool b_upd = bnd && (!b_is_a || bw_own > Real(0));   // one-way: a is never moved
+    // grab anchors (_core.pyx:1002-1020): the world's grab slots that hold
+    // this point (slot order is the reference's order for several on one
+    // point); the phase exists when any slot is active
+    const bool grabs = A.any_grabs != 0;
+    uint32_t gmask = 0;
+    if (grabs && pv)
+        for (int gsl = 0; gsl < A.ngrab; ++gsl)
+            if (A.g_act[gsl] && A.g_pt[gsl] == pt) gmask |= 1u << gsl;
 
     int cur = 0;   // state buffer of this exchange period
     int jp = 0;    // step within the period
@@ -552,7 +560,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         // last barrier, and then this CTA alone replays its sweeps from the
         // post-gather velocities with the IEEE division for such lanes (one
         // warp-uniform test per phase) -- its neighbours are unaffected.
-        const int iters = (BIND || A.any_dist) ? A.iters : 0;
+        const int iters = (BIND || grabs || A.any_dist) ? A.iters : 0;
         const Real v_g[3] = {v[0], v[1], v[2]};
         auto sweeps = [&](auto careful_c) -> int {
             constexpr bool CAREFUL = decltype(careful_c)::value;
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1 && c == 1 && !BIND) any_noted = __syncthreads_or(noted);
+                    if (!CAREFUL && it == 1 && c == 1 && !BIND && !grabs) any_noted = __syncthreads_or(noted);
                     else __syncthreads();
                 }
                 if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
@@ -612,6 +620,34 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     }
 #pragma unroll
                     for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * lam * bn[k]);
+                    vb_off = HL_VA + HL_VB - vb_off;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+                    if (!CAREFUL && it == 1 && !grabs) any_noted = __syncthreads_or(noted);
+                    else __syncthreads();
+                }
+                if (grabs) {   // grab anchors, start-of-step positions, slot order
+                    uint32_t gm = gmask;
+                    while (gm) {
+                        const int gsl = __ffs(gm) - 1;
+                        gm &= gm - 1;
+                        const Real wbv = im;
+                        if (wbv == Real(0)) continue;
+                        Real d[3], gn[3];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) d[k] = p[k] - A.g_tgt[3 * gsl + k];
+                        const Real dist = norm3(d);
+                        if (dist == Real(0)) continue;
+                        Real vrel = Real(0.0);
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            gn[k] = d[k] / dist;
+                            vrel = vrel + v[k] * gn[k];
+                        }
+                        const Real lam = -(vrel + beta * dist / dt) / wbv;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) v[k] = v[k] + wbv * lam * gn[k];
+                    }
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];

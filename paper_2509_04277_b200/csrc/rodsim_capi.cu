@@ -1728,7 +1728,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // the wide-halo kernel takes the launch of an eligible group (no grabs,
     // not live, ghost width still covering the iterations); a failed vote is
     // replayed exactly by resolve_halo at the next synchronisation
-    const bool halo = !exact && g.halo && h->halo_on && h->h_grabs.empty() && !h->live && cfg0 < 3 &&
+    const bool halo = !exact && g.halo && h->halo_on && !h->live && cfg0 < 3 &&
                       (g.h_g == g.h_s || g.h_s * (2 * h->d.iters + 1) <= g.h_g) && t_cnt < 0;
     if (halo) {
         if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 2), h->st));

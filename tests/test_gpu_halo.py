@@ -208,12 +208,27 @@ def test_more_iterations_than_the_ghost_width_bitwise():
     assert_bitwise(g, r)
 
 
-def test_grab_falls_back_to_the_general_kernel_bitwise():
-    def make():
-        w = wl.sweep(1024)
-        w.grab(0, 700, (1.5, 0.05, 0.0))
-        return w
-    halo_run(make, 60, 20)
+def test_grabs_bitwise():
+    # grab anchors on the wide-halo kernel: two slots on one point (slot
+    # order), one on an owned boundary point, a release mid-run
+    def script(world, run):
+        s1 = world.grab(0, 700, (1.5, 0.05, 0.0))
+        # a second slot on the same point (the world's arrays directly)
+        world.grab_point[5] = world.grab_point[s1]
+        world.grab_target[5] = (1.4, 0.02, 0.01)
+        world.grab_active[5] = 1
+        world.grab(0, 64, (0.1, 0.03, 0.0))   # CTA 0's last owned point, CTA 1's ghost
+        run(40)
+        world.release(0, 700)
+        run(30)
+
+    g, r = wl.sweep(1024), wl.sweep(1024)
+    with Engine(g) as eng:
+        assert eng.plan()["groups"][0]["halo"]
+        script(g, eng.run_epoch)
+        assert eng.device_world.last_redo_count() == 0
+    script(r, OracleStepper(r).run)
+    assert_bitwise(g, r)
 
 
 def test_tolerance_modes():
