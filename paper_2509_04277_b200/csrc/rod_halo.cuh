@@ -174,6 +174,29 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const int R1 = sweeps ? 2 * A.iters + 1 : 1;
     const bool m_ga0 = pv && dout <= S * R1 - 1;   // statics used by the first step's sweeps
 
+    // barrier wait accounting (the reference's per-block barrier_wait_ns,
+    // _core.pyx:453-471; A.bar_cycles non-null for the parallel backend):
+    // thread 0 of every CTA adds the SM cycles it spends in the step's barriers
+    const bool btime = t == 0 && A.bar_cycles != nullptr;
+    unsigned long long bwait = 0;
+    auto csync = [&]() {   // a CTA barrier
+        const long long tb = btime ? clock64() : 0;
+        __syncthreads();
+        if (btime) bwait += (unsigned long long)(clock64() - tb);
+    };
+    auto csync_or = [&](int pred) -> int {
+        const long long tb = btime ? clock64() : 0;
+        const int r_ = __syncthreads_or(pred);
+        if (btime) bwait += (unsigned long long)(clock64() - tb);
+        return r_;
+    };
+    auto xsync = [&]() {   // the step's exchange barrier
+        const long long tb = btime ? clock64() : 0;
+        if (ncl > 1) cluster_barrier();
+        else __syncthreads();
+        if (btime) bwait += (unsigned long long)(clock64() - tb);
+    };
+
     // neighbours' thread index of a pushed point (same W everywhere)
     const bool has_l = rank > 0, has_r = rank + 1 < ncl;
     const int x0_l = has_l ? A.htask[rank - 1].x0 : 0;
@@ -257,11 +280,52 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     // grab anchors (_core.pyx:1002-1020): the world's grab slots that hold
     // this point (slot order is the reference's order for several on one
     // point); the phase exists when any slot is active
-    const bool grabs = A.any_grabs != 0;
+    bool grabs = A.any_grabs != 0;
     uint32_t gmask = 0;
     if (grabs && pv)
         for (int gsl = 0; gsl < A.ngrab; ++gsl)
             if (A.g_act[gsl] && A.g_pt[gsl] == pt) gmask |= 1u << gsl;
+
+    // Live launches (one cluster, S = 1; ph_boundary, _core.pyx:477-506):
+    // the drainer (rank 0, thread 0) applies the ring rows it saw -- its read
+    // of the ring's tail is issued a step ahead -- just before the cluster
+    // barrier that ends a step, stamping the next step as their apply step,
+    // and bumps a generation word in every CTA's shared memory; after the
+    // barrier the CTAs reload their driver values and grab slots, so a command
+    // takes effect at the same step everywhere.  Per-step snapshots
+    // (ph_publish, _core.pyx:1045-1052): owned points written into the
+    // unpublished buffer, published by the drainer after the barrier.
+    const bool LIVE = A.live != nullptr;
+    const bool drainer = LIVE && rank == 0 && t == 0;
+    volatile int32_t* ctl =
+        reinterpret_cast<volatile int32_t*>(smem_raw + align16(size_t(HL_NF) * size_t(T) * sizeof(Real)) + 4);
+    int64_t live_head = 0, live_seen = 0;
+    int32_t my_gen = 0, live_gen = 0;
+    auto reload = [&]() {
+        if (drp >= 0)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dvel[k] = A.drv_v_live[3 * drp + k];
+        if (drf >= 0) drot = A.drv_rot_live[drf];
+        bool anyg = false;
+        gmask = 0;
+        for (int gsl = 0; gsl < A.ngrab; ++gsl) {
+            const bool a = A.g_act[gsl] != 0;
+            anyg = anyg || a;
+            if (a && pv && A.g_pt[gsl] == pt) gmask |= 1u << gsl;
+        }
+        grabs = anyg;
+    };
+    if (LIVE) {   // the rows staged before the launch apply at its first step
+        if (t == 0) *ctl = 0;
+        if (drainer) {
+            live_head = *reinterpret_cast<volatile int64_t*>(&A.live->head);
+            live_seen = ld_acquire_sys(&A.live->tail);
+            if (live_seen > live_head) live_head = live_drain(A, live_head, A.step0);
+        }
+        if (ncl > 1) cluster_barrier();
+        else __syncthreads();
+        reload();
+    }
 
     int cur = 0;   // state buffer of this exchange period
     int jp = 0;    // step within the period
@@ -291,8 +355,11 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) HS(sb + HL_Q + k, t) = q[k];
-            __syncthreads();
+            csync();
         }
+
+        int64_t live_next = 0;
+        if (drainer) live_next = ld_relaxed_sys(&A.live->tail);   // used at this step's end
 
         // ============ scatter (_core.pyx:745-805): element i ============
         Real pb[3], vb[3], qb[4], wb[3];
@@ -454,7 +521,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
 #pragma unroll
         for (int k = 0; k < 4; ++k) HS(HL_FN + k, t) = fn[k];
         HS(HL_B, t) = bias;
-        __syncthreads();
+        csync();
 
         // ============ gather (_core.pyx:808-875): point i, frame i ============
         Real efl[3], fnl[4], jtl[3], nn_l[3];
@@ -569,7 +636,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             int any_noted = 0;
 #pragma unroll
             for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-            __syncthreads();
+            csync();
             int rem = B - 1;   // radius still to come after the current phase
             for (int it = iters; it > 0; --it) {
 #pragma unroll
@@ -601,8 +668,8 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1 && c == 1 && !BIND && !grabs) any_noted = __syncthreads_or(noted);
-                    else __syncthreads();
+                    if (!CAREFUL && it == 1 && c == 1 && !BIND && !grabs) any_noted = csync_or(noted);
+                    else csync();
                 }
                 if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
                     Real vrel = Real(0.0);
@@ -623,8 +690,8 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1 && !grabs) any_noted = __syncthreads_or(noted);
-                    else __syncthreads();
+                    if (!CAREFUL && it == 1 && !grabs) any_noted = csync_or(noted);
+                    else csync();
                 }
                 if (grabs) {   // grab anchors, start-of-step positions, slot order
                     uint32_t gm = gmask;
@@ -651,13 +718,14 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1) any_noted = __syncthreads_or(noted);
-                    else __syncthreads();
+                    if (!CAREFUL && it == 1) any_noted = csync_or(noted);
+                    else csync();
                 }
             }
             return any_noted;
         };
         if (iters > 0 && sweeps(std::false_type{})) {
+            if (A.debug & 4) why |= 256u;   // (debug: a careful replay happened)
 #pragma unroll
             for (int k = 0; k < 3; ++k) v[k] = v_g[k];
             sweeps(std::true_type{});
@@ -685,6 +753,28 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             for (int k = 0; k < 4; ++k) q[k] = qn[k];
         }
 
+        if (LIVE) {
+            if (A.snap && own) {   // this step's snapshot into the unpublished buffer
+                const int64_t wbuf = (A.snap_base + step + 1) & 1;
+                double* sp = A.snap_pos + wbuf * 3 * A.snap_P;
+                double* sq = A.snap_q + wbuf * 4 * A.snap_E;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) sp[3 * size_t(pt) + k] = double(p[k]);
+                if (ev)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) sq[4 * size_t(el) + k] = double(q[k]);
+            }
+            if (drainer) {   // the next step's commands, before the barrier ending this one
+                if (step + 1 < A.steps && live_seen > live_head) {
+                    live_head = live_drain(A, live_head, A.step0 + step + 1);
+                    ++live_gen;
+                    for (unsigned c = 0; c < ncl; ++c)
+                        *cg::this_cluster().map_shared_rank(const_cast<int32_t*>(ctl), c) = live_gen;
+                }
+                live_seen = live_next;
+            }
+        }
+
         // ===== exchange (every S steps): owned boundary state to the neighbours =====
         const bool xs = jp == S - 1 && step + 1 < A.steps;
         jp = xs ? 0 : jp + 1;
@@ -705,7 +795,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             };
             if (push_l) gput(mine, i - tk.o0);                    // side 0: for the left neighbour
             if (push_r) gput(mine + hrec, i - (tk.o1 - G));       // side 1: for the right one
-            __syncthreads();
+            csync();
             if (t == 0) {
                 __threadfence();
                 st_release_gpu(A.flags + rank, nx);
@@ -714,7 +804,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                 if (has_r)
                     while (ld_acquire_gpu(A.flags + rank + 1) < nx) {}
             }
-            __syncthreads();
+            csync();
             if (pv && !own) {
                 const bool left = i < tk.o0;
                 const Real* src = A.halo + (size_t(par) * ncl + (left ? rank - 1 : rank + 1)) * 2 * hrec +
@@ -746,8 +836,18 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             if (own) put(sm, t);
             if (push_l) put(sm_l, t_l);
             if (push_r) put(sm_r, t_r);
-            if (ncl > 1) cluster_barrier();
-            else __syncthreads();
+            xsync();
+        }
+        if (LIVE && step + 1 < A.steps) {   // (live launches exchange every step)
+            if (A.snap && drainer) {        // the step's snapshot: every CTA's writes are done
+                const int64_t ver = A.snap_base + step + 1;
+                *reinterpret_cast<volatile int64_t*>(&A.snap->step[ver & 1]) = A.step0 + step + 1;
+                st_release_sys(&A.snap->pub, ver);
+            }
+            if (*ctl != my_gen) {   // commands applied for the next step
+                my_gen = *ctl;
+                reload();
+            }
         }
     }
 
@@ -774,6 +874,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         any = __syncthreads_or(any);
         cluster_barrier();   // every remote read done before a CTA exits
     }
+    if (LIVE && A.snap && drainer) {   // the last step's snapshot
+        const int64_t ver = A.snap_base + A.steps;
+        *reinterpret_cast<volatile int64_t*>(&A.snap->step[ver & 1]) = A.step0 + A.steps;
+        st_release_sys(&A.snap->pub, ver);
+    }
+    if (btime && bwait) atomicAdd(A.bar_cycles, bwait);
     if ((A.debug & 4) && why && A.prof) atomicOr(A.prof + PROF_SLOTS - 1, (unsigned long long)why);
 #undef OKC
     if (any) {   // nothing written back: the host replays this launch exactly

@@ -498,10 +498,12 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
         // 3.93 us/step, 256: 6.23 -> 3.97, 512: 9.59 -> 4.06; the 64-element
         // cantilever stays on its CTA, 3.80 vs 3.91).  RSB_HALO_CTA: 0 never,
         // 1 at any size
-        const bool cta_ok = g.tier == TIER_CTA && g.ncta == 1 && h->halo_cta != 0 &&
+        // (two tasks: two equal rods, one per CTA -- the same column layout
+        // as a bound pair, without the bindings)
+        const bool cta_ok = g.tier == TIER_CTA && g.ncta <= 2 && h->halo_cta != 0 &&
                             (h->halo_cta == 1 || h->h_tasks[g.task_begin].np >= kHaloCtaMinPoints);
         if ((g.tier != TIER_CLUSTER && g.tier != TIER_GRID && !cta_ok) || g.uni != 2 || !h->halo_on ||
-            h->contacts_on || d.has_self || d.live || d.force_ctas > 0 || d.force_variant >= 0)
+            h->contacts_on || d.has_self || d.force_ctas > 0 || d.force_variant >= 0)
             continue;
         const CtaTask& tf = h->h_tasks[g.task_begin];
         const CtaTask& tl = h->h_tasks[g.task_begin + g.ncta - 1];
@@ -551,38 +553,18 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
         // one per colour phase; without distance-projected elements or
         // bindings there are no sweeps)
         const int R1 = (g.any_dist || bind) ? int(2 * d.iters + 1) : 1;
-        // one cluster of up to 16 CTAs while its CTAs stay within 256
-        // threads (no spills); beyond, or on request, a co-resident grid of
-        // CTAs of ~halo_width threads (more, thinner CTAs: a phase's issue
-        // per SM is what bounds its latency)
-        const int m_cl = int((np + kMaxCluster - 1) / kMaxCluster);
-        bool gx = h->halo_grid == 1 || (h->halo_grid != 0 && nr * (m_cl + 2 * R1) > 256);
-        // steps per exchange: the grid's exchange (an L2 round trip, 1-4 us)
-        // is amortised over kHaloGridSteps steps (cfg4 N = 16384, S = 1 / 2 / 3:
-        // 11.1 / 8.5 / 7.3 us per step; N = 8192: 9.8 / 7.5 / 7.1); a cluster
-        // barrier is worth wider ghosts only when they are one point per step
-        // (no colour sweeps: cfg2 3.80 -> 3.67 us at S = 2)
-        const int S = h->halo_steps > 0 ? h->halo_steps : (gx ? kHaloGridSteps : (R1 == 1 ? 2 : 1));
-        const int G = S * R1;
-        int C;
-        if (!gx) {
-            C = h->halo_ctas > 0 ? h->halo_ctas : kMaxCluster;
-            C = std::min(C, kMaxCluster);
-        } else {
-            // (wider CTAs once the grid passes ~96 CTAs: cfg4 N = 16384 at
-            // 128 / 192 / 256 threads: 10.7 / 9.7 / 9.5 us per step)
-            int width = h->halo_width;
-            auto ctas_for = [&](int wdt) {
-                const int m_t = std::max(G, wdt / nr - 2 * G);
-                return int((np + m_t - 1) / m_t);
-            };
-            while (h->halo_ctas <= 0 && ctas_for(width) > 96 && width < 256) width += 32;
-            C = h->halo_ctas > 0 ? h->halo_ctas : ctas_for(width);
-            C = std::min(C, h->num_sms > 0 ? h->num_sms : 148);
-        }
-        C = int(std::min<int64_t>(C, np / G));
-        if (C < 1) continue;
-        auto layout = [&](int c, std::vector<HaloTask>& ts, int& wmax) {
+        // Layout candidates, first feasible wins: one cluster of up to 16
+        // CTAs while they stay within 256 threads (no spills); else a
+        // co-resident grid of CTAs of ~halo_width threads (more, thinner
+        // CTAs: a phase's issue per SM is what bounds its latency); else a
+        // cluster of up to 512-thread CTAs.  Steps per exchange S: the grid's
+        // exchange (an L2 round trip, 1-4 us) is amortised over up to
+        // kHaloGridSteps steps while the ghosts stay within ~96 points
+        // (cfg4 N = 16384, S = 1 / 2 / 3: 11.1 / 8.5 / 7.3 us per step; N = 8192:
+        // 9.8 / 7.5 / 7.1); a cluster barrier is worth wider ghosts only when
+        // they are one point per step (no colour sweeps: cfg2 3.80 -> 3.67 us
+        // at S = 2).  Live launches: one cluster, an exchange every step.
+        auto layout = [&](int c, int G, std::vector<HaloTask>& ts, int& wmax) {
             ts.clear();
             wmax = 0;
             const int64_t base = np / c, rem = np % c;
@@ -599,11 +581,68 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
                 o += sz;
             }
         };
-        std::vector<HaloTask> ts;
-        int wmax = 0;
-        layout(C, ts, wmax);
-        const int threads = (nr * wmax + 31) / 32 * 32;
-        if (threads > 512) continue;
+        struct Cand {
+            bool gx;
+            int S, G, C, threads, wmax;
+            std::vector<HaloTask> ts;
+        };
+        auto make_cand = [&](bool cgx) -> Cand {
+            Cand c{};
+            c.gx = cgx;
+            c.S = h->live ? 1 : h->halo_steps > 0 ? h->halo_steps
+                              : cgx ? std::max(1, std::min(kHaloGridSteps, 96 / R1)) : (R1 == 1 ? 2 : 1);
+            c.G = c.S * R1;
+            int C;
+            if (!cgx) {
+                C = h->halo_ctas > 0 ? h->halo_ctas : kMaxCluster;
+                C = std::min(C, kMaxCluster);
+            } else {
+                // (wider CTAs once the grid passes ~96 CTAs: cfg4 N = 16384 at
+                // 128 / 192 / 256 threads: 10.7 / 9.7 / 9.5 us per step)
+                int width = h->halo_width;
+                auto ctas_for = [&](int wdt) {
+                    const int m_t = std::max(c.G, wdt / nr - 2 * c.G);
+                    return int((np + m_t - 1) / m_t);
+                };
+                while (h->halo_ctas <= 0 && ctas_for(width) > 96 && width < 256) width += 32;
+                C = h->halo_ctas > 0 ? h->halo_ctas : ctas_for(width);
+                C = std::min(C, h->num_sms > 0 ? h->num_sms : 148);
+            }
+            c.C = int(std::min<int64_t>(C, np / c.G));
+            if (c.C < 1) {
+                c.threads = 1 << 30;
+                return c;
+            }
+            layout(c.C, c.G, c.ts, c.wmax);
+            c.threads = (nr * c.wmax + 31) / 32 * 32;
+            return c;
+        };
+        std::vector<Cand> cands;
+        if (h->halo_grid == 1 && !h->live) {
+            cands.push_back(make_cand(true));
+        } else if (h->halo_grid == 0 || h->live) {
+            cands.push_back(make_cand(false));
+        } else {
+            Cand cl = make_cand(false);
+            if (cl.threads <= 256) {
+                cands.push_back(cl);
+            } else {
+                Cand gr = make_cand(true);
+                if (gr.threads < cl.threads) cands.push_back(gr);   // (thinner CTAs than the cluster's)
+                cands.push_back(cl);
+                cands.push_back(gr);
+            }
+        }
+        const Cand* pick = nullptr;
+        for (const Cand& c : cands)
+            if (c.threads <= 512 && (c.gx ? c.C >= 2 : c.C <= kMaxCluster)) {
+                pick = &c;
+                break;
+            }
+        if (!pick) continue;
+        const bool gx = pick->gx;
+        const int S = pick->S, G = pick->G, C = pick->C, threads = pick->threads, wmax = pick->wmax;
+        const std::vector<HaloTask>& ts = pick->ts;
         g.h_tasks = ts;
         g.h_gx = gx;
         g.h_cta = C;
@@ -1728,7 +1767,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // the wide-halo kernel takes the launch of an eligible group (no grabs,
     // not live, ghost width still covering the iterations); a failed vote is
     // replayed exactly by resolve_halo at the next synchronisation
-    const bool halo = !exact && g.halo && h->halo_on && !h->live && cfg0 < 3 &&
+    const bool halo = !exact && g.halo && h->halo_on &&
                       (g.h_g == g.h_s || g.h_s * (2 * h->d.iters + 1) <= g.h_g) && t_cnt < 0;
     if (halo) {
         if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 2), h->st));
@@ -2186,7 +2225,8 @@ int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* ba
     const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 && !h->contacts_on &&
                            !h->d.has_mesh && !h->d.has_self &&
                            (h->groups[0].tier == TIER_CTA || h->groups[0].tier == TIER_STREAM) &&
-                           h->groups[0].ncta >= 2 && steps <= kMaxStepsPerLaunch;
+                           h->groups[0].ncta >= 2 && steps <= kMaxStepsPerLaunch &&
+                           !(h->groups[0].halo && h->halo_on);   // (a wide-halo launch covers the group)
     if (!pipelined) {
         int rc = upload_state(h);
         if (rc) return rc;

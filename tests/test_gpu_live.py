@@ -124,3 +124,41 @@ def test_live_snapshots_during_an_epoch_match_the_oracle():
         o.run(s.step_index - r.step_index)
         assert np.array_equal(_bits(s.positions), _bits(r.positions)), s.step_index
         assert np.array_equal(_bits(s.frames), _bits(r.frames)), s.step_index
+
+
+def test_live_grab_release_and_driver_on_the_wide_halo_kernel():
+    # a 1024-element rod on the wide-halo kernel (one cluster, an exchange
+    # barrier per step): a grab near a CTA boundary, a driver, then the
+    # release, all posted mid-epoch; each lands at a step boundary in every
+    # CTA at once
+    steps = 8000
+
+    def make():   # (no gravity: the rod rests, the grab pulls 1 mm)
+        w = wl.sweep(1024)
+        w.gravity[:] = 0.0
+        w.set_driver(0)
+        return w
+
+    def post(eng):
+        assert eng.plan()["groups"][0]["halo"]
+        time.sleep(0.005)
+        a = eng.post_command("grab", rod=0, index=700, target=(1.4, 1e-3, 0.0))
+        time.sleep(0.004)
+        b = eng.post_command("insert_velocity", rod=0, value=0.05, axis=(0.0, 1.0, 0.0))
+        time.sleep(0.004)
+        c = eng.post_command("release", rod=0, index=700)
+        return [a, b, c]
+    g, (s_grab, s_drv, s_rel) = live_run(make, steps, post)
+    assert 1 < s_grab <= s_drv <= s_rel < 1 + steps
+    r = make()
+    o = OracleStepper(r)
+    o.run(s_grab)
+    r.grab(0, 700, np.array([1.4, 1e-3, 0.0]))
+    o.run(s_drv - s_grab)
+    r.driver_velocity[0] = (0.0, 0.05, 0.0)
+    o.run(s_rel - s_drv)
+    r.release(0, 700)
+    o.run(1 + steps - s_rel)
+    assert np.isfinite(r.positions).all()
+    for k in STATE:
+        assert np.array_equal(_bits(getattr(g, k)), _bits(getattr(r, k))), k

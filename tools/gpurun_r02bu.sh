@@ -1,0 +1,1 @@
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/r02bu_pytest_gpu.log 2>&1; echo pytest=$?; tail -4 gpurun_out/r02bu_pytest_gpu.log
