@@ -121,7 +121,10 @@ __device__ __forceinline__ void hl_div(const R (&a)[N], R b, R rb, bool b_ok, bo
 // double-buffered global halo record per CTA and side, published with a
 // release flag per CTA that the two neighbours acquire -- still one exchange
 // per step.
-template <typename Real, int MODE, bool GEN, bool BIND, int TB, bool GX>
+// XF: grab anchors, live launches (kernel-side ring drain, snapshots) and
+// barrier-wait accounting compiled in -- a plain launch carries none of it
+// (with the code present but idle, cfg4 N = 256 ran 4.2 -> 4.7 us per step).
+template <typename Real, int MODE, bool GEN, bool BIND, int TB, bool GX, bool XF>
 __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -176,20 +179,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
 
     // barrier wait accounting (the reference's per-block barrier_wait_ns,
     // _core.pyx:453-471; A.bar_cycles non-null for the parallel backend):
-    // thread 0 of every CTA adds the SM cycles it spends in the step's barriers
-    const bool btime = t == 0 && A.bar_cycles != nullptr;
+    // thread 0 of every CTA adds the SM cycles it waits at the inter-CTA
+    // exchange barrier -- the reference's inter-block barrier; the phases'
+    // CTA barriers stay untimed (a clock read around each sat on the chain)
+    const bool btime = XF && t == 0 && A.bar_cycles != nullptr;
     unsigned long long bwait = 0;
-    auto csync = [&]() {   // a CTA barrier
-        const long long tb = btime ? clock64() : 0;
-        __syncthreads();
-        if (btime) bwait += (unsigned long long)(clock64() - tb);
-    };
-    auto csync_or = [&](int pred) -> int {
-        const long long tb = btime ? clock64() : 0;
-        const int r_ = __syncthreads_or(pred);
-        if (btime) bwait += (unsigned long long)(clock64() - tb);
-        return r_;
-    };
+    auto csync = [&]() { __syncthreads(); };
+    auto csync_or = [&](int pred) -> int { return __syncthreads_or(pred); };
     auto xsync = [&]() {   // the step's exchange barrier
         const long long tb = btime ? clock64() : 0;
         if (ncl > 1) cluster_barrier();
@@ -280,7 +276,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     // grab anchors (_core.pyx:1002-1020): the world's grab slots that hold
     // this point (slot order is the reference's order for several on one
     // point); the phase exists when any slot is active
-    bool grabs = A.any_grabs != 0;
+    bool grabs = XF && A.any_grabs != 0;
     uint32_t gmask = 0;
     if (grabs && pv)
         for (int gsl = 0; gsl < A.ngrab; ++gsl)
@@ -295,7 +291,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     // takes effect at the same step everywhere.  Per-step snapshots
     // (ph_publish, _core.pyx:1045-1052): owned points written into the
     // unpublished buffer, published by the drainer after the barrier.
-    const bool LIVE = A.live != nullptr;
+    const bool LIVE = XF && A.live != nullptr;
     const bool drainer = LIVE && rank == 0 && t == 0;
     volatile int32_t* ctl =
         reinterpret_cast<volatile int32_t*>(smem_raw + align16(size_t(HL_NF) * size_t(T) * sizeof(Real)) + 4);
@@ -638,7 +634,16 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
             csync();
             int rem = B - 1;   // radius still to come after the current phase
-            for (int it = iters; it > 0; --it) {
+            // one iteration; the fast sweeps' last phase ends at an OR-barrier
+            // that collects the notes (the last iteration is peeled, so no
+            // phase tests which barrier to take)
+            auto iteration = [&](auto last_c) {
+                constexpr bool LAST = decltype(last_c)::value;
+                // the iteration's final phase: odd colour, binding or grab
+                auto end_phase = [&](bool final_) {
+                    if (!CAREFUL && LAST && final_) any_noted = csync_or(noted);
+                    else csync();
+                };
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     --rem;
@@ -661,15 +666,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                             if (off) lam = div_ieee(-(x + Real(0.0)), wsP[c]);
                     } else {
                         noted = noted | off;
-                        if (A.debug & 4) why |= off ? 32u : 0u;
                     }
 #pragma unroll
                     for (int k = 0; k < 3; ++k) sub_if(actP[c], v[k], im * lam * nP[c][k]);
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1 && c == 1 && !BIND && !grabs) any_noted = csync_or(noted);
-                    else csync();
+                    end_phase(c == 1 && !BIND && !grabs);
                 }
                 if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
                     Real vrel = Real(0.0);
@@ -683,17 +686,15 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                             if (off) lam = div_ieee(-(vrel + bbias), bws);
                     } else {
                         noted = noted | off;
-                        if (A.debug & 4) why |= off ? 64u : 0u;
                     }
 #pragma unroll
                     for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * lam * bn[k]);
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1 && !grabs) any_noted = csync_or(noted);
-                    else csync();
+                    end_phase(!grabs);
                 }
-                if (grabs) {   // grab anchors, start-of-step positions, slot order
+                if (XF && grabs) {   // grab anchors, start-of-step positions, slot order
                     uint32_t gm = gmask;
                     while (gm) {
                         const int gsl = __ffs(gm) - 1;
@@ -718,14 +719,19 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    if (!CAREFUL && it == 1) any_noted = csync_or(noted);
-                    else csync();
+                    end_phase(true);
                 }
+            };
+            if constexpr (CAREFUL) {
+                for (int it = iters; it > 0; --it) iteration(std::false_type{});
+            } else {
+                for (int it = iters; it > 1; --it) iteration(std::false_type{});
+                iteration(std::true_type{});
             }
             return any_noted;
         };
         if (iters > 0 && sweeps(std::false_type{})) {
-            if (A.debug & 4) why |= 256u;   // (debug: a careful replay happened)
+            if (A.debug & 4) why |= 256u | 32u;   // (debug: a careful replay happened)
 #pragma unroll
             for (int k = 0; k < 3; ++k) v[k] = v_g[k];
             sweeps(std::true_type{});

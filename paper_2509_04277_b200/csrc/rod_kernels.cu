@@ -19,7 +19,7 @@ template cudaError_t occupancy<RSB_REAL>(int, int, int, int, size_t, int, int*);
 #if !RSB_FEAT
 template cudaError_t batch_step<RSB_REAL>(int, int, const StepArgs<RSB_REAL>*, int, cudaStream_t, int*);
 template cudaError_t warp_step<RSB_REAL>(int, int, const StepArgs<RSB_REAL>*, int, cudaStream_t);
-template cudaError_t halo_step<RSB_REAL>(int, int, int, int, int, const StepArgs<RSB_REAL>*, int, int,
+template cudaError_t halo_step<RSB_REAL>(int, int, int, int, int, int, const StepArgs<RSB_REAL>*, int, int,
                                          cudaStream_t, int*);
 #endif
 }  // namespace RSB_MODE_NS

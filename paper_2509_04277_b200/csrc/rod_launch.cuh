@@ -304,9 +304,9 @@ cudaError_t warp_step(int gen, int form, const StepArgs<Real>* a, int grid, cuda
 }
 
 // The wide-halo cluster kernel (rod_halo.cuh): one cluster of ncta CTAs.
-template <typename Real, bool GEN, bool BIND, int TB, bool GX>
+template <typename Real, bool GEN, bool BIND, int TB, bool GX, bool XF>
 static cudaError_t halo_one(int what, const StepArgs<Real>* a, int ncta, int threads, cudaStream_t st, int* out) {
-    auto fn = rod_halo_kernel<Real, RSB_MODE_ID, GEN, BIND, TB, GX>;
+    auto fn = rod_halo_kernel<Real, RSB_MODE_ID, GEN, BIND, TB, GX, XF>;
     static std::atomic<bool> done[64];
     cudaError_t e = configure_once(fn, done);
     if (e != cudaSuccess) return e;
@@ -350,14 +350,14 @@ static cudaError_t halo_one(int what, const StepArgs<Real>* a, int ncta, int thr
     return cudaLaunchKernelEx(&cfg, fn, *a);
 }
 // what: 0 launch, 1 occupancy query (cluster: active clusters, grid: CTAs
-// per SM); tb: 256 or 512; gx: grid exchange instead of one cluster
-template <typename Real>
-cudaError_t halo_step(int what, int gen, int bind, int tb, int gx, const StepArgs<Real>* a, int ncta, int threads,
-                      cudaStream_t st, int* out) {
-    const int sel = (gen ? 1 : 0) | (bind ? 2 : 0) | (tb > 256 ? 4 : 0) | (gx ? 8 : 0);
+// per SM); tb: 256 or 512; gx: grid exchange instead of one cluster; xf:
+// grabs / live launches / barrier accounting compiled in
+template <typename Real, bool XF>
+static cudaError_t halo_sel(int what, int sel, const StepArgs<Real>* a, int ncta, int threads, cudaStream_t st,
+                            int* out) {
     switch (sel) {
 #define RSB_H(S, G, B, T, X) \
-    case S: return halo_one<Real, G, B, T, X>(what, a, ncta, threads, st, out);
+    case S: return halo_one<Real, G, B, T, X, XF>(what, a, ncta, threads, st, out);
         RSB_H(0, false, false, 256, false)
         RSB_H(1, true, false, 256, false)
         RSB_H(2, false, true, 256, false)
@@ -377,6 +377,13 @@ cudaError_t halo_step(int what, int gen, int bind, int tb, int gx, const StepArg
 #undef RSB_H
     }
     return cudaErrorInvalidValue;
+}
+template <typename Real>
+cudaError_t halo_step(int what, int gen, int bind, int tb, int gx, int xf, const StepArgs<Real>* a, int ncta,
+                      int threads, cudaStream_t st, int* out) {
+    const int sel = (gen ? 1 : 0) | (bind ? 2 : 0) | (tb > 256 ? 4 : 0) | (gx ? 8 : 0);
+    return xf ? halo_sel<Real, true>(what, sel, a, ncta, threads, st, out)
+              : halo_sel<Real, false>(what, sel, a, ncta, threads, st, out);
 }
 
 // shape in [0, kBwNumShapes) with gen = false, or kBwNumShapes + shape for

@@ -42,7 +42,7 @@
     template <typename Real>                                                                       \
     cudaError_t warp_step(int, int, const StepArgs<Real>*, int, cudaStream_t);                    \
     template <typename Real>                                                                       \
-    cudaError_t halo_step(int, int, int, int, int, const StepArgs<Real>*, int, int, cudaStream_t, int*); \
+    cudaError_t halo_step(int, int, int, int, int, int, const StepArgs<Real>*, int, int, cudaStream_t, int*); \
     }                                                                                              \
     }
 RSB_DECLARE_MODE(mirror)
@@ -1629,11 +1629,11 @@ int halo_query(rs_handle h, const Group& g, int* out) {
     cudaError_t e;
     const int gen = g.h_gen ? 1 : 0, bind = g.h_bind ? 1 : 0;
     if (h->prec == RS_F64_MIRROR)
-        e = mirror::halo_step<double>(1, gen, bind, g.h_tb, g.h_gx, nullptr, g.h_cta, g.h_threads, nullptr, out);
+        e = mirror::halo_step<double>(1, gen, bind, g.h_tb, g.h_gx, 1, nullptr, g.h_cta, g.h_threads, nullptr, out);
     else if (h->prec == RS_F32)
-        e = f32::halo_step<float>(1, gen, bind, g.h_tb, g.h_gx, nullptr, g.h_cta, g.h_threads, nullptr, out);
+        e = f32::halo_step<float>(1, gen, bind, g.h_tb, g.h_gx, 1, nullptr, g.h_cta, g.h_threads, nullptr, out);
     else
-        e = f64fast::halo_step<double>(1, gen, bind, g.h_tb, g.h_gx, nullptr, g.h_cta, g.h_threads, nullptr, out);
+        e = f64fast::halo_step<double>(1, gen, bind, g.h_tb, g.h_gx, 1, nullptr, g.h_cta, g.h_threads, nullptr, out);
     if (e != cudaSuccess) {
         cudaGetLastError();
         *out = 0;   // not launchable here: the group keeps the general kernel
@@ -1772,6 +1772,8 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     if (halo) {
         if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 2), h->st));
         const int gen = (g.h_gen || h->has_fext) ? 1 : 0, bind = g.h_bind ? 1 : 0;
+        // grabs, live launches, barrier accounting: the XF kernels
+        const int xf = (!h->h_grabs.empty() || h->live || h->bar_timing) ? 1 : 0;
         // the halo launch's own exchange buffers
         auto hx = [&](auto a) {
             a.flags = g.d_hflags;
@@ -1781,13 +1783,13 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         cudaError_t eh;
         if (h->prec == RS_F64_MIRROR) {
             auto a = hx(make_args<double>(h, g, step0, steps));
-            eh = mirror::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &a, g.h_cta, g.h_threads, h->st, nullptr);
+            eh = mirror::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, xf, &a, g.h_cta, g.h_threads, h->st, nullptr);
         } else if (h->prec == RS_F32) {
             auto a = hx(make_args<float>(h, g, step0, steps));
-            eh = f32::halo_step<float>(0, gen, bind, g.h_tb, g.h_gx, &a, g.h_cta, g.h_threads, h->st, nullptr);
+            eh = f32::halo_step<float>(0, gen, bind, g.h_tb, g.h_gx, xf, &a, g.h_cta, g.h_threads, h->st, nullptr);
         } else {
             auto a = hx(make_args<double>(h, g, step0, steps));
-            eh = f64fast::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, &a, g.h_cta, g.h_threads, h->st, nullptr);
+            eh = f64fast::halo_step<double>(0, gen, bind, g.h_tb, g.h_gx, xf, &a, g.h_cta, g.h_threads, h->st, nullptr);
         }
         if (eh != cudaSuccess)
             return fail(RS_E_CUDA, "wide-halo launch (%d CTAs x %d threads) failed: %s", g.h_cta, g.h_threads,
