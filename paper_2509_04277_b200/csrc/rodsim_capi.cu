@@ -204,6 +204,9 @@ struct rs_handle_s {
     int halo_width = 128;           // RSB_HALO_W: target threads per CTA of the grid exchange
     int halo_steps = 0;             // RSB_HALO_STEPS: steps per exchange (0: the planner's)
     bool halo_pending = false;      // wide-halo launches not yet checked for a failed vote
+    bool halo_check_enqueued = false;   // their redo words are on the way to h_hfail
+    int64_t* h_hfail = nullptr;     // pinned, one per group
+    size_t h_hfail_n = 0;
     bool last_halo = false;         // the last launch was a wide-halo launch
     int64_t halo_redone = 0;        // groups replayed exactly at the last check
     int halo_cta = -1;              // RSB_HALO_CTA: one-CTA segments (-1: from kHaloCtaMinPoints)
@@ -1822,16 +1825,39 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
 // current one.  Called before anything reads or replaces the device state
 // or changes what a replay would compute (synchronisation, download, upload,
 // staged commands, parameters).
-int resolve_halo(rs_handle h) {
-    if (!h->halo_pending) return RS_OK;
+// The groups' redo words come back to pinned host memory with one
+// asynchronous copy each (enqueue_halo_check), read after a synchronisation
+// the caller does anyway (finish_halo_check): a download costs no extra
+// round trip in the common case.
+int enqueue_halo_check(rs_handle h) {
+    if (!h->halo_pending || h->halo_check_enqueued) return RS_OK;
+    const size_t ng = h->groups.size();
+    if (h->h_hfail_n < ng) {
+        if (h->h_hfail) cudaFreeHost(h->h_hfail);
+        h->h_hfail = nullptr;
+        CK(cudaMallocHost(&h->h_hfail, sizeof(int64_t) * ng));
+        h->h_hfail_n = ng;
+    }
+    for (size_t gi = 0; gi < ng; ++gi) {
+        h->h_hfail[gi] = 0;
+        if (h->groups[gi].d_hfail)
+            CK(cudaMemcpyAsync(h->h_hfail + gi, h->groups[gi].d_hfail, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               h->st));
+    }
+    h->halo_check_enqueued = true;
+    return RS_OK;
+}
+// after a synchronisation of h->st: replay failed groups; *replayed: any
+int finish_halo_check(rs_handle h, bool* replayed) {
+    if (replayed) *replayed = false;
+    if (!h->halo_check_enqueued) return RS_OK;
+    h->halo_check_enqueued = false;
     h->halo_pending = false;
     int64_t redone = 0;
-    for (const Group& g : h->groups) {
-        if (!g.d_hfail) continue;
-        int64_t v = 0;
-        CK(cudaMemcpyAsync(&v, g.d_hfail, sizeof v, cudaMemcpyDeviceToHost, h->st));
-        CK(cudaStreamSynchronize(h->st));
-        if (!v) continue;
+    for (size_t gi = 0; gi < h->groups.size(); ++gi) {
+        const Group& g = h->groups[gi];
+        const int64_t v = h->h_hfail[gi];
+        if (!g.d_hfail || !v) continue;
         CK(cudaMemsetAsync(g.d_hfail, 0, sizeof(int64_t), h->st));
         const bool lh = h->last_halo;
         for (int64_t s0 = v - 1; s0 < h->step;) {
@@ -1844,7 +1870,15 @@ int resolve_halo(rs_handle h) {
         ++redone;
     }
     h->halo_redone = redone;
+    if (replayed) *replayed = redone > 0;
     return RS_OK;
+}
+int resolve_halo(rs_handle h) {
+    if (!h->halo_pending) return RS_OK;
+    int rc = enqueue_halo_check(h);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(h->st));
+    return finish_halo_check(h, nullptr);
 }
 
 void register_host(rs_handle h, void* p, size_t bytes) {
@@ -2175,7 +2209,8 @@ int download_control(rs_handle h) {
 int rs_download(rs_handle h, uint32_t mask) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     CK(cudaSetDevice(h->d.device));
-    if (int rc = resolve_halo(h)) return rc;
+    // the redo words travel with the state; a replay (rare) downloads again
+    if (int rc = enqueue_halo_check(h)) return rc;
     const rs_world_desc& d = h->d;
     int rc = RS_OK;
     if ((mask & (RS_STATE | RS_CONTROL)) && h->live && h->planned)
@@ -2215,6 +2250,12 @@ int rs_download(rs_handle h, uint32_t mask) {
             if ((rc = get_real(h, h->cacc_n, d.cacc_n, P))) return rc;
             if ((rc = get_real(h, h->cacc_t, d.cacc_t, P))) return rc;
         }
+    }
+    if (h->halo_check_enqueued) {
+        CK(cudaStreamSynchronize(h->st));
+        bool replayed = false;
+        if ((rc = finish_halo_check(h, &replayed))) return rc;
+        if (replayed) return rs_download(h, mask);
     }
     return rs_synchronize(h);
 }
@@ -2366,6 +2407,7 @@ void rs_destroy(rs_handle h) {
     for (cudaEvent_t e : h->redo_ev)
         if (e) cudaEventDestroy(e);
     if (h->h_redo) cudaFreeHost(h->h_redo);
+    if (h->h_hfail) cudaFreeHost(h->h_hfail);
     if (h->d_prof && (h->debug & 4)) {   // wide-halo failed checks (RSB_DEBUG bit 2)
         unsigned long long v = 0;
         if (cudaMemcpy(&v, h->d_prof + PROF_SLOTS - 1, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
