@@ -334,6 +334,8 @@ def latency_floor(plan, us, k, lat, iters=10, ext=False, t_launch_us=0.0):
     n_sync = plan["sync_per_step"]
     t_sync = barrier_ns(plan)
     halo = plan.get("halo")
+    if halo and halo.get("short_epochs_only") and k >= 32:
+        halo = None   # (long epochs of such rods run the speculative CTA kernel)
     if halo:
         # wide-halo kernel (rod_halo.cuh): every phase ends at a CTA barrier
         # of halo["threads"], the step at one inter-CTA exchange (cluster

@@ -72,11 +72,21 @@ __device__ __forceinline__ void closest_tri(const Real p[3], const Real a[3], co
     for (int k = 0; k < 3; ++k) out[k] = a[k] + ab[k] * (vb * denom) + ac[k] * (vc * denom);
 }
 
-// Detection for global point p with centre `center` (start-of-step position).
-// Writes the contact slot (cnorm, cdepth, cact = 1) when the sphere touches
-// the mesh; returns true for a degenerate (zero-area) triangle met.
+// A point's contact slot (_core.pyx:730-741) held in registers (the wide-halo
+// kernel keeps one per thread; the general kernel's slots live in global
+// memory, the wrappers below).
 template <typename Real>
-__device__ __noinline__ bool mesh_contact(const StepArgs<Real>& A, int64_t p, const Real center[3]) {
+struct ContactSlot {
+    Real n[3], depth, acc_n, acc_t;
+    bool act;
+};
+
+// Detection for global point p with centre `center` (start-of-step position):
+// on a hit the slot's normal and depth are set and act = true (a miss leaves
+// the slot alone); returns true for a degenerate (zero-area) triangle met.
+template <typename Real>
+__device__ __noinline__ bool mesh_detect(const StepArgs<Real>& A, int64_t p, const Real center[3],
+                                         ContactSlot<Real>& cs) {
     int stack[CONTACT_STACK];
     const Real radius = A.cradii[p] + A.coll_margin;
     Real lo[3], hi[3], wsum[3] = {Real(0), Real(0), Real(0)}, best[3] = {Real(0), Real(0), Real(0)};
@@ -149,34 +159,49 @@ __device__ __noinline__ bool mesh_contact(const StepArgs<Real>& A, int64_t p, co
     if (nhits == 0) return degenerate;
     const Real norm = sqrt(wsum[0] * wsum[0] + wsum[1] * wsum[1] + wsum[2] * wsum[2]);
     if (norm < Real(1e-12) * (maxd > Real(1.0) ? maxd : Real(1.0))) {
-        for (int k = 0; k < 3; ++k) A.cnorm[3 * p + k] = best[k];
+        for (int k = 0; k < 3; ++k) cs.n[k] = best[k];
     } else {
-        for (int k = 0; k < 3; ++k) A.cnorm[3 * p + k] = wsum[k] / norm;
+        for (int k = 0; k < 3; ++k) cs.n[k] = wsum[k] / norm;
     }
     maxd = maxd - A.coll_margin;   // the margin inflates detection only
     if (maxd < Real(0)) maxd = Real(0);
-    A.cdepth[p] = maxd;
-    A.cact[p] = 1;
+    cs.depth = maxd;
+    cs.act = true;
+    return degenerate;
+}
+
+// The same writing the global slot of point p (cnorm, cdepth, cact = 1).
+template <typename Real>
+__device__ __noinline__ bool mesh_contact(const StepArgs<Real>& A, int64_t p, const Real center[3]) {
+    ContactSlot<Real> cs;
+    cs.act = false;
+    const bool degenerate = mesh_detect(A, p, center, cs);
+    if (cs.act) {
+        for (int k = 0; k < 3; ++k) A.cnorm[3 * p + k] = cs.n[k];
+        A.cdepth[p] = cs.depth;
+        A.cact[p] = 1;
+    }
     return degenerate;
 }
 
 // Normal impulse with accumulator, then box friction, on the velocity v of
-// an unlocked point with an active contact (_core.pyx:906-947).
+// an unlocked point with an active contact (_core.pyx:906-947), slot in
+// registers.
 template <typename Real>
-__device__ __forceinline__ void contact_impulse(const StepArgs<Real>& A, int64_t p, Real m, Real v[3]) {
+__device__ __forceinline__ void contact_impulse_r(const StepArgs<Real>& A, Real m, Real v[3], ContactSlot<Real>& cs) {
     Real n[3], vt[3];
     Real vn = Real(0);
     for (int k = 0; k < 3; ++k) {
-        n[k] = A.cnorm[3 * p + k];
+        n[k] = cs.n[k];
         vn = vn + v[k] * n[k];
     }
-    const Real raw = m * ((-vn) * (Real(1.0) + A.restitution) + (A.beta * A.cdepth[p]) / A.dt);
-    const Real acc = A.cacc_n[p];
+    const Real raw = m * ((-vn) * (Real(1.0) + A.restitution) + (A.beta * cs.depth) / A.dt);
+    const Real acc = cs.acc_n;
     Real new_acc = acc + raw;
     if (new_acc < Real(0)) new_acc = Real(0);
     const Real applied = new_acc - acc;
     for (int k = 0; k < 3; ++k) v[k] = v[k] + (applied / m) * n[k];
-    A.cacc_n[p] = new_acc;
+    cs.acc_n = new_acc;
     if (A.mu > Real(0)) {
         Real dot = Real(0), vt_norm = Real(0);
         for (int k = 0; k < 3; ++k) dot = dot + v[k] * n[k];
@@ -185,7 +210,7 @@ __device__ __forceinline__ void contact_impulse(const StepArgs<Real>& A, int64_t
             vt_norm = vt_norm + vt[k] * vt[k];
         }
         vt_norm = sqrt(vt_norm);
-        Real cap = A.mu * new_acc - A.cacc_t[p];
+        Real cap = A.mu * new_acc - cs.acc_t;
         if (cap < Real(0)) cap = Real(0);
         Real jt = m * vt_norm;
         if (jt > cap) jt = cap;
@@ -193,8 +218,21 @@ __device__ __forceinline__ void contact_impulse(const StepArgs<Real>& A, int64_t
             const Real scale = jt / (m * vt_norm);
             for (int k = 0; k < 3; ++k) v[k] = v[k] - scale * vt[k];
         }
-        A.cacc_t[p] = A.cacc_t[p] + jt;
+        cs.acc_t = cs.acc_t + jt;
     }
+}
+// ... on point p's global slot
+template <typename Real>
+__device__ __forceinline__ void contact_impulse(const StepArgs<Real>& A, int64_t p, Real m, Real v[3]) {
+    ContactSlot<Real> cs;
+    for (int k = 0; k < 3; ++k) cs.n[k] = A.cnorm[3 * p + k];
+    cs.depth = A.cdepth[p];
+    cs.acc_n = A.cacc_n[p];
+    cs.acc_t = A.cacc_t[p];
+    cs.act = true;
+    contact_impulse_r(A, m, v, cs);
+    A.cacc_n[p] = cs.acc_n;
+    if (A.mu > Real(0)) A.cacc_t[p] = cs.acc_t;
 }
 
 // The impulse on a velocity held in shared memory, out of line: the contact

@@ -65,10 +65,12 @@ namespace rsb {
 
 // the state fields (double-buffered) and the per-step fields, T Reals each
 enum HaloField : int {
-    HL_P = 0, HL_V = 3, HL_Q = 6, HL_W = 10, HL_NSTATE = 13,   // x 2 (parity)
-    HL_EF = 26, HL_FN = 29, HL_JT = 33, HL_NN = 36, HL_B = 39,  // scatter outputs
-    HL_VA = 40, HL_VB = 43,                                      // colour ping-pong
-    HL_NF = 46,
+    HL_P = 0, HL_V = 3, HL_Q = 6, HL_W = 10,                    // x 2 (parity)
+    HL_CA = 13, HL_CN = 14, HL_CD = 17,                          // contact slot (mesh scenes)
+    HL_NSTATE = 18,
+    HL_EF = 36, HL_FN = 39, HL_JT = 43, HL_NN = 46, HL_B = 49,  // scatter outputs
+    HL_VA = 50, HL_VB = 53,                                      // colour ping-pong
+    HL_NF = 56,
 };
 __host__ __device__ constexpr size_t halo_smem_bytes(int threads, size_t rsz) {
     return align16(size_t(HL_NF) * size_t(threads) * rsz) + 16;
@@ -311,6 +313,24 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         }
         grabs = anyg;
     };
+    // mesh contacts (_core.pyx:509-662 detection, 906-947 impulses): every
+    // thread keeps its point's contact slot in registers (ghosts too, like
+    // the rest of the state: detection reads the step-start position, the
+    // impulse phase is radius 0); the slots travel with the ghost exchange
+    // and the owners write them back
+    const bool CONT = XF && A.contacts_on != 0;
+    ContactSlot<Real> cs;
+    cs.act = false;
+    cs.depth = cs.acc_n = cs.acc_t = Real(0);
+    cs.n[0] = cs.n[1] = cs.n[2] = Real(0);
+    if (CONT && pv) {
+        cs.act = A.cact[pt] != 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) cs.n[k] = A.cnorm[3 * size_t(pt) + k];
+        cs.depth = A.cdepth[pt];
+        cs.acc_n = A.cacc_n[pt];
+        cs.acc_t = A.cacc_t[pt];
+    }
     if (LIVE) {   // the rows staged before the launch apply at its first step
         if (t == 0) *ctl = 0;
         if (drainer) {
@@ -341,6 +361,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) q[k] = HS(sb + HL_Q + k, t);
+            if (CONT) {
+                cs.act = HS(sb + HL_CA, t) != Real(0);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) cs.n[k] = HS(sb + HL_CN + k, t);
+                cs.depth = HS(sb + HL_CD, t);
+            }
         }
         if (step == 0 || GX || jp > 0) {
 #pragma unroll
@@ -356,6 +382,14 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
 
         int64_t live_next = 0;
         if (drainer) live_next = ld_relaxed_sys(&A.live->tail);   // used at this step's end
+        if (CONT) {   // contact slots: reset, detection on collision steps (_core.pyx:730-741)
+            cs.acc_n = Real(0);
+            cs.acc_t = Real(0);
+            if ((A.step0 + step) % A.coll_interval == 0) {
+                cs.act = false;
+                if (pv && A.has_mesh && A.cmask[pt]) OKC(512, !(mesh_detect(A, int64_t(pt), p, cs) & m_ga));
+            }
+        }
 
         // ============ scatter (_core.pyx:745-805): element i ============
         Real pb[3], vb[3], qb[4], wb[3];
@@ -623,7 +657,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         // last barrier, and then this CTA alone replays its sweeps from the
         // post-gather velocities with the IEEE division for such lanes (one
         // warp-uniform test per phase) -- its neighbours are unaffected.
-        const int iters = (BIND || grabs || A.any_dist) ? A.iters : 0;
+        const int iters = (BIND || grabs || CONT || A.any_dist) ? A.iters : 0;
         const Real v_g[3] = {v[0], v[1], v[2]};
         auto sweeps = [&](auto careful_c) -> int {
             constexpr bool CAREFUL = decltype(careful_c)::value;
@@ -672,7 +706,14 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    end_phase(c == 1 && !BIND && !grabs);
+                    end_phase(c == 1 && !CONT && !BIND && !grabs);
+                }
+                if (CONT) {   // contact impulses (_core.pyx:906-947), radius 0
+                    if (cs.act && !pl) contact_impulse_r(A, m, v, cs);
+                    vb_off = HL_VA + HL_VB - vb_off;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
+                    end_phase(!BIND && !grabs);
                 }
                 if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
                     Real vrel = Real(0.0);
@@ -731,6 +772,10 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
             return any_noted;
         };
         if (iters > 0 && sweeps(std::false_type{})) {
+            if (CONT) {   // (the step's accumulators start at zero)
+                cs.acc_n = Real(0);
+                cs.acc_t = Real(0);
+            }
             if (A.debug & 4) why |= 256u | 32u;   // (debug: a careful replay happened)
 #pragma unroll
             for (int k = 0; k < 3; ++k) v[k] = v_g[k];
@@ -798,6 +843,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) x[HL_Q + k] = q[k];
+                if (CONT) {
+                    x[HL_CA] = cs.act ? Real(1) : Real(0);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) x[HL_CN + k] = cs.n[k];
+                    x[HL_CD] = cs.depth;
+                }
             };
             if (push_l) gput(mine, i - tk.o0);                    // side 0: for the left neighbour
             if (push_r) gput(mine + hrec, i - (tk.o1 - G));       // side 1: for the right one
@@ -825,6 +876,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) q[k] = ld_halo(x + HL_Q + k);
+                if (CONT) {
+                    cs.act = ld_halo(x + HL_CA) != Real(0);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) cs.n[k] = ld_halo(x + HL_CN + k);
+                    cs.depth = ld_halo(x + HL_CD);
+                }
             }
         } else if (!GX && xs) {
             cur ^= 1;
@@ -838,6 +895,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) base[(nb + HL_Q + k) * T + x] = q[k];
+                if (CONT) {
+                    base[(nb + HL_CA) * T + x] = cs.act ? Real(1) : Real(0);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) base[(nb + HL_CN + k) * T + x] = cs.n[k];
+                    base[(nb + HL_CD) * T + x] = cs.depth;
+                }
             };
             if (own) put(sm, t);
             if (push_l) put(sm_l, t_l);
@@ -891,6 +954,15 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     if (any) {   // nothing written back: the host replays this launch exactly
         if (rank == 0 && t == 0) *A.hfail = A.step0 + 1;
         return;
+    }
+    if (CONT && own) {   // the contact slots; epoch_results' count after the last step
+        A.cact[pt] = cs.act ? 1 : 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) A.cnorm[3 * size_t(pt) + k] = cs.n[k];
+        A.cdepth[pt] = cs.depth;
+        A.cacc_n[pt] = cs.acc_n;
+        A.cacc_t[pt] = cs.acc_t;
+        if (cs.act) atomicAdd(A.contacts, 1ull);
     }
     if (own) {
 #pragma unroll

@@ -150,6 +150,7 @@ struct Group {       // one kernel launch
     int h_s = 1;                    // steps per ghost exchange (ghost width h_s (2I+1))
     int32_t h_poff[2] = {0, 0}, h_eoff[2] = {0, 0};
     bool h_gx = false;              // grid exchange (co-resident grid) instead of one cluster
+    bool h_short = false;           // only for epochs shorter than kSpecMinSteps
     std::vector<HaloTask> h_tasks;
     HaloTask* d_htask = nullptr;
     int32_t* d_hflags = nullptr;    // grid exchange: per-CTA flags, arrival count, vote OR
@@ -164,6 +165,7 @@ struct Group {       // one kernel launch
 // a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
 constexpr int kSpecMinSteps = 32;
 constexpr int kHaloCtaMinPoints = 100;
+constexpr int kHaloCtaShortPoints = 40;
 constexpr int kHaloGridSteps = 3;
 constexpr int kSpecBackoff = 64;
 bool spec_group(const Group& g) {
@@ -503,10 +505,16 @@ int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vecto
         // 1 at any size
         // (two tasks: two equal rods, one per CTA -- the same column layout
         // as a bound pair, without the bindings)
+        // Smaller one-CTA rods (>= kHaloCtaShortPoints) take it only for
+        // epochs shorter than kSpecMinSteps, where the speculative CTA kernel
+        // does not run (cfg1, 65 points, K = 1 / 10: 7.04 / 4.28 -> 6.55 / 4.17
+        // us per step; K = 100: 3.80 vs 3.98)
+        const int cta_np = h->h_tasks[g.task_begin].np;
         const bool cta_ok = g.tier == TIER_CTA && g.ncta <= 2 && h->halo_cta != 0 &&
-                            (h->halo_cta == 1 || h->h_tasks[g.task_begin].np >= kHaloCtaMinPoints);
+                            (h->halo_cta == 1 || cta_np >= kHaloCtaShortPoints);
+        g.h_short = g.tier == TIER_CTA && h->halo_cta != 1 && cta_np < kHaloCtaMinPoints;
         if ((g.tier != TIER_CLUSTER && g.tier != TIER_GRID && !cta_ok) || g.uni != 2 || !h->halo_on ||
-            h->contacts_on || d.has_self || d.force_ctas > 0 || d.force_variant >= 0)
+            d.has_self || d.force_ctas > 0 || d.force_variant >= 0)
             continue;
         const CtaTask& tf = h->h_tasks[g.task_begin];
         const CtaTask& tl = h->h_tasks[g.task_begin + g.ncta - 1];
@@ -1770,13 +1778,13 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // the wide-halo kernel takes the launch of an eligible group (no grabs,
     // not live, ghost width still covering the iterations); a failed vote is
     // replayed exactly by resolve_halo at the next synchronisation
-    const bool halo = !exact && g.halo && h->halo_on &&
+    const bool halo = !exact && g.halo && h->halo_on && (!g.h_short || steps < kSpecMinSteps) &&
                       (g.h_g == g.h_s || g.h_s * (2 * h->d.iters + 1) <= g.h_g) && t_cnt < 0;
     if (halo) {
         if (g.h_gx) CK(cudaMemsetAsync(g.d_hflags, 0, sizeof(int32_t) * size_t(g.h_cta + 2), h->st));
         const int gen = (g.h_gen || h->has_fext) ? 1 : 0, bind = g.h_bind ? 1 : 0;
         // grabs, live launches, barrier accounting: the XF kernels
-        const int xf = (!h->h_grabs.empty() || h->live || h->bar_timing) ? 1 : 0;
+        const int xf = (!h->h_grabs.empty() || h->live || h->bar_timing || h->contacts_on) ? 1 : 0;
         // the halo launch's own exchange buffers
         auto hx = [&](auto a) {
             a.flags = g.d_hflags;
@@ -2534,8 +2542,9 @@ int rs_plan_json(rs_handle h, char* buf, int64_t len) {
         char hj[200] = "null";
         if (g.halo)
             snprintf(hj, sizeof hj, "{\"ctas\": %d, \"threads\": %d, \"ghost\": %d, \"rods\": %d, \"bindings\": %s, "
-                     "\"exchange\": \"%s\", \"steps_per_exchange\": %d}",
-                     g.h_cta, g.h_threads, g.h_g, g.h_nr, g.h_bind ? "true" : "false", g.h_gx ? "grid" : "cluster", g.h_s);
+                     "\"exchange\": \"%s\", \"steps_per_exchange\": %d, \"short_epochs_only\": %s}",
+                     g.h_cta, g.h_threads, g.h_g, g.h_nr, g.h_bind ? "true" : "false", g.h_gx ? "grid" : "cluster", g.h_s,
+                     g.h_short ? "true" : "false");
         char tmp[1200];
         snprintf(tmp, sizeof tmp,
                  "%s{\"tier\": \"%s\", \"variant\": %d, \"slots_per_thread\": %d, \"cap\": %d, "

@@ -206,12 +206,13 @@ def test_plan_wide_halo_kernel():
         return plan(w, **kw)[0]["halo"]
     h = halo(wl.pair())
     assert h == {"ctas": 16, "threads": 160, "ghost": 21, "rods": 2, "bindings": True, "exchange": "cluster",
-                 "steps_per_exchange": 1}
+                 "steps_per_exchange": 1, "short_epochs_only": False}
     assert halo(wl.extensible())["ghost"] == 2          # no colour sweeps: radius 1, 2 steps
     assert halo(wl.sweep(16384))["steps_per_exchange"] == 3
     assert halo(wl.sweep(16384))["exchange"] == "grid"
     assert halo(wl.sweep(256))["exchange"] == "cluster"
-    assert halo(wl.cantilever()) is None
+    assert halo(wl.cantilever())["short_epochs_only"]          # K < 32 only (65 points)
+    assert halo(wl.sweep(16)) is None
     assert halo(wl.sweep(1024), force_tier=1, force_ctas=4) is None
     assert halo(wl.hair(2048)) is None
     w = wl.pair()
