@@ -151,6 +151,7 @@ struct Group {       // one kernel launch
     int32_t h_poff[2] = {0, 0}, h_eoff[2] = {0, 0};
     bool h_gx = false;              // grid exchange (co-resident grid) instead of one cluster
     bool h_short = false;           // only for epochs shorter than kSpecMinSteps
+    bool halo_only = false;         // no general kernel can step the group (coupled, past a cluster)
     std::vector<HaloTask> h_tasks;
     HaloTask* d_htask = nullptr;
     int32_t* d_hflags = nullptr;    // grid exchange: per-CTA flags, arrival count, vote OR
@@ -487,7 +488,17 @@ int halo_query(rs_handle h, const Group& g, int* out);
 // owns ~np / C consecutive local indices plus G = 2I + 1 ghost points per
 // side; the planner takes the largest cluster (<= 16) whose CTAs own at least
 // G points each.
+int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std::vector<int32_t>& pt_elem);
 int plan_halo(rs_handle h, const std::vector<uint32_t>& pflags, const std::vector<int32_t>& pt_elem) {
+    int rc = plan_halo_groups(h, pflags, pt_elem);
+    if (rc) return rc;
+    for (const Group& g : h->groups)
+        if (g.halo_only && !g.halo)
+            return fail(RS_E_UNSUPPORTED, "coupled rods larger than a %d-CTA cluster need the wide-halo kernel "
+                        "(two equal rods bound at the same local index, launch-uniform material)", kMaxCluster);
+    return RS_OK;
+}
+int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std::vector<int32_t>& pt_elem) {
     const rs_world_desc& d = h->d;
     const int64_t P = d.P;
     h->h_hdrv.assign(size_t(2 * P), -1);
@@ -792,6 +803,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                                                                  : kCtaMaxPoints;
     const int clu_cap = kVariants[kNumCapVariants - 1].cover();
     std::vector<int> seg_tier(segs.size());
+    std::vector<char> seg_halo_only(segs.size(), 0);
     int64_t max_cta_seg = 0;
     for (size_t i = 0; i < segs.size(); ++i) {
         const int64_t np = segs[i].p1 - segs[i].p0;
@@ -809,9 +821,12 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
                         (long long)np);
         if (tier == TIER_CTA && np > cta_cap)
             return fail(RS_E_INVALID, "segment of %lld points does not fit one CTA", (long long)np);
-        if (tier == TIER_GRID) {
-            if (segs[i].r0 != segs[i].r1)
+        // coupled rods past one cluster: the wide-halo kernel's grid exchange
+        // only (the general grid tier cannot bind across CTAs)
+        if (tier == TIER_GRID && segs[i].r0 != segs[i].r1) {
+            if (!h->halo_on || d.force_tier >= 0)
                 return fail(RS_E_UNSUPPORTED, "coupled rods larger than a %d-CTA cluster", kMaxCluster);
+            seg_halo_only[i] = 1;
         }
         seg_tier[i] = tier;
         if (tier == TIER_CTA) max_cta_seg = std::max(max_cta_seg, np);
@@ -931,6 +946,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         }
         g.ncta = c;
         g.cluster = g.tier == TIER_CLUSTER ? c : 1;
+        g.halo_only = seg_halo_only[i] != 0;
         h->groups.push_back(g);
     }
 
@@ -1175,7 +1191,7 @@ int plan(rs_handle h, std::vector<uint32_t>& pflags, std::vector<int32_t>& pt_el
         if (rc) return rc;
         if (g.tier == TIER_CLUSTER && occ < 1)
             return fail(RS_E_UNSUPPORTED, "a %d-CTA cluster of %zu B smem cannot be resident", g.cluster, g.smem);
-        if (g.tier == TIER_GRID && int64_t(occ) * h->num_sms < g.ncta)
+        if (g.tier == TIER_GRID && !g.halo_only && int64_t(occ) * h->num_sms < g.ncta)
             return fail(RS_E_UNSUPPORTED, "grid tier needs %d co-resident CTAs, device holds %d", g.ncta,
                         occ * h->num_sms);
         if ((g.tier == TIER_CTA || g.tier == TIER_STREAM) && occ < 1)
@@ -1812,6 +1828,11 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         return RS_OK;
     }
     h->last_halo = false;
+    if (g.halo_only)
+        return fail(RS_E_UNSUPPORTED, exact ? "wide-halo launch failed (degenerate geometry or non-finite forces) on "
+                                              "coupled rods past one cluster: no exact fallback"
+                                            : "coupled rods past one cluster need the wide-halo kernel (RSB_HALO, "
+                                              "iterations beyond the planned ghost width)");
     cudaError_t e = bw ? one_bw() : rw ? one_rw() : (spec ? one(cfg0 + 6, 0) : one(cfg0, 0));
     if (e == cudaSuccess && spec) e = one(cfg0, 1);
     if (e == cudaSuccess && spec && backoff && !h->redo_ev_live[gi]) {

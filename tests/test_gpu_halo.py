@@ -242,3 +242,22 @@ def test_tolerance_modes():
         L = 2e-3 * 1024
         assert np.max(np.abs(g.positions - r.positions)) <= tol_r * L
         assert np.max(np.abs(g.frames - r.frames)) <= (1e-4 if prec == "f32" else 1e-9)
+
+
+def test_coupled_pair_past_one_cluster_bitwise():
+    # 2 x 9500 bound points exceed a 16-CTA cluster: the general planner
+    # rejected such sets; the wide-halo grid exchange steps them
+    make = lambda: wl.pair(9500, 19.0)   # noqa: E731
+    _, grp, redo = halo_run(make, 9, 3)
+    assert grp["tier"] == "grid" and grp["halo"]["exchange"] == "grid" and grp["halo"]["rods"] == 2
+    assert redo == 0
+
+
+def test_coupled_pair_past_one_cluster_has_no_exact_fallback():
+    # a degenerate segment fails the vote; no general kernel can replay such
+    # a set, so the download reports it instead of returning unstepped state
+    w = wl.pair(9500, 19.0)
+    w.positions[101] = w.positions[100]
+    with Engine(w) as eng:
+        with pytest.raises(NotImplementedError, match="no exact fallback"):
+            eng.run_epoch(3)
