@@ -719,9 +719,16 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     Real vrel = Real(0.0);
 #pragma unroll
                     for (int k = 0; k < 3; ++k) vrel = vrel + (HS(vb_off + k, t_b) - v[k]) * bn[k];
-                    bool lok = true;
-                    Real lam = hl_quot(-(vrel + bbias), bws, brws, lok);
-                    const bool off = bact & (dout <= rem) & !lok;
+                    // the colour phases' quotient: vrel and bias are never
+                    // -0 (vrel starts from +0, the bias is >= 0), so a zero
+                    // dividend gives -0 like the reference's -(vrel + bias) / ws;
+                    // anything outside the window is noted for the careful pass
+                    const Real x = vrel + bbias;
+                    const Real q0 = (-x) * brws;
+                    Real lam = fma(fma(-q0, bws, -x), brws, q0);
+                    const bool z = is_zero(x);
+                    if (z) lam = Real(-0.0);
+                    const bool off = bact & (dout <= rem) & !(in_window(x) | z);
                     if constexpr (CAREFUL) {
                         if (__any_sync(0xffffffffu, off))
                             if (off) lam = div_ieee(-(vrel + bbias), bws);
