@@ -141,7 +141,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const unsigned ncl = gridDim.x;   // one cluster (or one co-resident grid) per launch
     const HaloTask tk = A.htask[rank];
     const int NR = A.h_nr, W = A.h_w, np = A.h_np, ne = np - 1;
-    const int r = t / W, j = t - r * W;
+    // bound rods interleaved: thread t = 2 j + r holds point j of rod r, so a
+    // bound column's two points sit on adjacent lanes of one warp and the
+    // binding takes its partner by shuffle; otherwise rod r's points are the
+    // threads r W .. r W + W - 1.  ST: the thread distance of neighbouring
+    // points of a rod (a compile-time constant on every neighbour access).
+    constexpr int ST = BIND ? 2 : 1;
+    const int r = BIND ? (t & 1) : t / W, j = BIND ? (t >> 1) : t - (t / W) * W;
     const int i = tk.x0 + j;                        // local index along the rod
     const bool pv = r < NR && i < tk.x1;            // thread holds a point
     const bool ev = pv && i < ne;                   // ... and its element
@@ -210,7 +216,8 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     }
     // grid exchange: one side's record = NR x G points x 13 state words
     const size_t hrec = size_t(NR) * size_t(G) * HL_NSTATE;
-    const int t_l = r * W + (i - x0_l), t_r = r * W + (i - x0_r);
+    const int t_l = BIND ? 2 * (i - x0_l) + r : r * W + (i - x0_l);
+    const int t_r = BIND ? 2 * (i - x0_r) + r : r * W + (i - x0_r);
 
     // ---- state and statics ----
     Real p[3], v[3], q[4], w[3];
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     // colour c: the element of colour c containing point i -- its own
     // (lower end) when i % 2 == c, the left one (upper end) otherwise
     const bool a_side[2] = {(i & 1) == 0, (i & 1) == 1};
-    const int partner[2] = {(i & 1) ? t - 1 : t + 1, (i & 1) ? t + 1 : t - 1};
+    const int partner[2] = {(i & 1) ? t - ST : t + ST, (i & 1) ? t + ST : t - ST};
     Real wsP[2], rwsP[2];
     bool actP[2];
 #pragma unroll
@@ -263,7 +270,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const int hb = (BIND && pv) ? A.hbind[pt] : -1;
     const bool bnd = hb >= 0;
     const bool b_is_a = (hb & 1) != 0;
-    const int t_b = (1 - rr) * W + j;
+    const int t_b = t ^ 1;   // (NR == 2)
     Real bw_own = Real(0), bws = Real(0), brws = Real(0);
     if constexpr (BIND) {
         const Real im_o = bnd ? A.invm[A.h_poff[1 - rr] + i] : Real(0);
@@ -395,12 +402,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         Real pb[3], vb[3], qb[4], wb[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            pb[k] = HS(sb + HL_P + k, t + 1);
-            vb[k] = HS(sb + HL_V + k, t + 1);
-            wb[k] = HS(sb + HL_W + k, t + 1);
+            pb[k] = HS(sb + HL_P + k, t + ST);
+            vb[k] = HS(sb + HL_V + k, t + ST);
+            wb[k] = HS(sb + HL_W + k, t + ST);
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) qb[k] = HS(sb + HL_Q + k, t + 1);
+        for (int k = 0; k < 4; ++k) qb[k] = HS(sb + HL_Q + k, t + ST);
         Real d[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) d[k] = pb[k] - p[k];
@@ -557,13 +564,13 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         Real efl[3], fnl[4], jtl[3], nn_l[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            efl[k] = HS(HL_EF + k, t - 1);
-            jtl[k] = HS(HL_JT + k, t - 1);
-            nn_l[k] = HS(HL_NN + k, t - 1);
+            efl[k] = HS(HL_EF + k, t - ST);
+            jtl[k] = HS(HL_JT + k, t - ST);
+            nn_l[k] = HS(HL_NN + k, t - ST);
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) fnl[k] = HS(HL_FN + k, t - 1);
-        const Real bias_l = HS(HL_B, t - 1);
+        for (int k = 0; k < 4; ++k) fnl[k] = HS(HL_FN + k, t - ST);
+        const Real bias_l = HS(HL_B, t - ST);
         Real a_v[3], dvv[3], a_w[3], dww[3];
         slow = false;
         {
@@ -703,71 +710,68 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
                     }
 #pragma unroll
                     for (int k = 0; k < 3; ++k) sub_if(actP[c], v[k], im * lam * nP[c][k]);
-                    vb_off = HL_VA + HL_VB - vb_off;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    end_phase(c == 1 && !CONT && !BIND && !grabs);
-                }
-                if (CONT) {   // contact impulses (_core.pyx:906-947), radius 0
-                    if (cs.act && !pl) contact_impulse_r(A, m, v, cs);
-                    vb_off = HL_VA + HL_VB - vb_off;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    end_phase(!BIND && !grabs);
-                }
-                if constexpr (BIND) {   // bindings (_core.pyx:981-1001), after the odd colour
-                    Real vrel = Real(0.0);
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) vrel = vrel + (HS(vb_off + k, t_b) - v[k]) * bn[k];
-                    // the colour phases' quotient: vrel and bias are never
-                    // -0 (vrel starts from +0, the bias is >= 0), so a zero
-                    // dividend gives -0 like the reference's -(vrel + bias) / ws;
-                    // anything outside the window is noted for the careful pass
-                    const Real x = vrel + bbias;
-                    const Real q0 = (-x) * brws;
-                    Real lam = fma(fma(-q0, bws, -x), brws, q0);
-                    const bool z = is_zero(x);
-                    if (z) lam = Real(-0.0);
-                    const bool off = bact & (dout <= rem) & !(in_window(x) | z);
-                    if constexpr (CAREFUL) {
-                        if (__any_sync(0xffffffffu, off))
-                            if (off) lam = div_ieee(-(vrel + bbias), bws);
-                    } else {
-                        noted = noted | off;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * lam * bn[k]);
-                    vb_off = HL_VA + HL_VB - vb_off;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    end_phase(!grabs);
-                }
-                if (XF && grabs) {   // grab anchors, start-of-step positions, slot order
-                    uint32_t gm = gmask;
-                    while (gm) {
-                        const int gsl = __ffs(gm) - 1;
-                        gm &= gm - 1;
-                        const Real wbv = im;
-                        if (wbv == Real(0)) continue;
-                        Real d[3], gn[3];
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) d[k] = p[k] - A.g_tgt[3 * gsl + k];
-                        const Real dist = norm3(d);
-                        if (dist == Real(0)) continue;
-                        Real vrel = Real(0.0);
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            gn[k] = d[k] / dist;
-                            vrel = vrel + v[k] * gn[k];
+                    if (c == 1) {
+                        // The iteration's central phases (_core.pyx:906-1020:
+                        // contacts, bindings, grabs) are radius 0 along a rod
+                        // and a binding's partner is the adjacent lane, so they
+                        // run here, before the odd phase's one barrier.
+                        if (CONT) {   // contact impulses, own point
+                            if (cs.act && !pl) contact_impulse_r(A, m, v, cs);
                         }
-                        const Real lam = -(vrel + beta * dist / dt) / wbv;
+                        if constexpr (BIND) {   // bindings: the partner's post-odd velocity by shuffle
+                            Real vbp[3];
 #pragma unroll
-                        for (int k = 0; k < 3; ++k) v[k] = v[k] + wbv * lam * gn[k];
+                            for (int k = 0; k < 3; ++k) vbp[k] = __shfl_xor_sync(0xffffffffu, v[k], 1);
+                            Real vrel = Real(0.0);
+#pragma unroll
+                            for (int k = 0; k < 3; ++k) vrel = vrel + (vbp[k] - v[k]) * bn[k];
+                            // the colour phases' quotient: vrel and bias are never
+                            // -0 (vrel starts from +0, the bias is >= 0), so a zero
+                            // dividend gives -0 like the reference's
+                            // -(vrel + bias) / ws; outside the window: noted
+                            const Real xb = vrel + bbias;
+                            const Real qb0 = (-xb) * brws;
+                            Real blam = fma(fma(-qb0, bws, -xb), brws, qb0);
+                            const bool zb = is_zero(xb);
+                            if (zb) blam = Real(-0.0);
+                            const bool boff = bact & (dout <= rem) & !(in_window(xb) | zb);
+                            if constexpr (CAREFUL) {
+                                if (__any_sync(0xffffffffu, boff))
+                                    if (boff) blam = div_ieee(-(vrel + bbias), bws);
+                            } else {
+                                noted = noted | boff;
+                            }
+#pragma unroll
+                            for (int k = 0; k < 3; ++k) sub_if(bact & b_upd, v[k], bw_own * blam * bn[k]);
+                        }
+                        if (XF && grabs) {   // grab anchors, start-of-step positions, slot order
+                            uint32_t gm = gmask;
+                            while (gm) {
+                                const int gsl = __ffs(gm) - 1;
+                                gm &= gm - 1;
+                                const Real wbv = im;
+                                if (wbv == Real(0)) continue;
+                                Real d[3], gn[3];
+#pragma unroll
+                                for (int k = 0; k < 3; ++k) d[k] = p[k] - A.g_tgt[3 * gsl + k];
+                                const Real dist = norm3(d);
+                                if (dist == Real(0)) continue;
+                                Real gvrel = Real(0.0);
+#pragma unroll
+                                for (int k = 0; k < 3; ++k) {
+                                    gn[k] = d[k] / dist;
+                                    gvrel = gvrel + v[k] * gn[k];
+                                }
+                                const Real glam = -(gvrel + beta * dist / dt) / wbv;
+#pragma unroll
+                                for (int k = 0; k < 3; ++k) v[k] = v[k] + wbv * glam * gn[k];
+                            }
+                        }
                     }
                     vb_off = HL_VA + HL_VB - vb_off;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) HS(vb_off + k, t) = v[k];
-                    end_phase(true);
+                    end_phase(c == 1);
                 }
             };
             if constexpr (CAREFUL) {

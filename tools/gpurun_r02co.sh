@@ -1,0 +1,2 @@
+for r in 1 2; do for l in base new2; do python tools/ab_probe.py build/ab/$l.so; done; done
+timeout 1500 python -m pytest tests/test_gpu_halo.py tests/test_gpu_parity.py tests/test_gpu_mesh.py tests/test_gpu_live.py tests/test_gpu_acceptance.py -q -x > gpurun_out/r02co_pytest.log 2>&1; echo pytest=$?; tail -2 gpurun_out/r02co_pytest.log
