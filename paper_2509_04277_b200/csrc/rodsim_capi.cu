@@ -516,14 +516,16 @@ int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std
         // 1 at any size
         // (two tasks: two equal rods, one per CTA -- the same column layout
         // as a bound pair, without the bindings)
-        // Smaller one-CTA rods (>= kHaloCtaShortPoints) take it only for
-        // epochs shorter than kSpecMinSteps, where the speculative CTA kernel
-        // does not run (cfg1, 65 points, K = 1 / 10: 7.04 / 4.28 -> 6.55 / 4.17
-        // us per step; K = 100: 3.80 vs 3.98)
+        // Smaller one-CTA rods (kHaloCtaShortPoints .. kHaloCtaMinPoints)
+        // take it as ONE CTA, no ghosts (cfg4, K = 100: 96 points 4.04 ->
+        // 3.83 us per step, 64 elements 3.81 -> 3.75; K = 10: 4.23 -> 4.10,
+        // 4.19 -> 3.99); rods the one-warp kernels take (<= 63 elements)
+        // only for epochs shorter than kSpecMinSteps, where those do not run
         const int cta_np = h->h_tasks[g.task_begin].np;
         const bool cta_ok = g.tier == TIER_CTA && g.ncta <= 2 && h->halo_cta != 0 &&
                             (h->halo_cta == 1 || cta_np >= kHaloCtaShortPoints);
-        g.h_short = g.tier == TIER_CTA && h->halo_cta != 1 && cta_np < kHaloCtaMinPoints;
+        const bool one_cta = g.tier == TIER_CTA && h->halo_cta != 1 && cta_np < kHaloCtaMinPoints;
+        g.h_short = one_cta && g.rw;
         if ((g.tier != TIER_CLUSTER && g.tier != TIER_GRID && !cta_ok) || g.uni != 2 || !h->halo_on ||
             d.has_self || d.force_ctas > 0 || d.force_variant >= 0)
             continue;
@@ -616,7 +618,7 @@ int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std
             c.G = c.S * R1;
             int C;
             if (!cgx) {
-                C = h->halo_ctas > 0 ? h->halo_ctas : kMaxCluster;
+                C = h->halo_ctas > 0 ? h->halo_ctas : (one_cta ? 1 : kMaxCluster);
                 C = std::min(C, kMaxCluster);
             } else {
                 // (wider CTAs once the grid passes ~96 CTAs: cfg4 N = 16384 at

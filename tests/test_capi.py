@@ -127,13 +127,23 @@ def test_plan_rejects_inconsistent_layouts():
     w.junction_valid[-1] = True          # a junction past the rod end
     with pytest.raises(ValueError, match="junction_valid"):
         plan(w)
+    # coupled rods past one 16-CTA cluster: the wide-halo grid exchange
+    # steps two equal rods bound at the same local index; anything else is
+    # rejected (no general kernel binds across a grid)
     big = World()
     for _ in range(2):
         big.add_rod(st.init_rod(12000, 24.0), st.RodParams())
     big.finalize()
     big.add_bindings(0, 1, BIND_BIDIRECTIONAL, stride=100)
+    g = plan(big)[0]
+    assert g["tier"] == "grid" and g["halo"]["exchange"] == "grid" and g["halo"]["rods"] == 2
+    odd = World()
+    odd.add_rod(st.init_rod(12000, 24.0), st.RodParams())
+    odd.add_rod(st.init_rod(11000, 22.0), st.RodParams())
+    odd.finalize()
+    odd.add_bindings(0, 1, BIND_BIDIRECTIONAL, stride=100)
     with pytest.raises(NotImplementedError):
-        plan(big)
+        plan(odd)
 
 
 @pytest.mark.skipif(have_gpu(), reason="checks the no-device failure path")
@@ -211,7 +221,8 @@ def test_plan_wide_halo_kernel():
     assert halo(wl.sweep(16384))["steps_per_exchange"] == 3
     assert halo(wl.sweep(16384))["exchange"] == "grid"
     assert halo(wl.sweep(256))["exchange"] == "cluster"
-    assert halo(wl.cantilever())["short_epochs_only"]          # K < 32 only (65 points)
+    assert halo(wl.cantilever())["ctas"] == 1                   # one CTA, no ghosts (65 points)
+    assert halo(wl.sweep(48))["short_epochs_only"]             # the one-warp kernel for K >= 32
     assert halo(wl.sweep(16)) is None
     assert halo(wl.sweep(1024), force_tier=1, force_ctas=4) is None
     assert halo(wl.hair(2048)) is None
