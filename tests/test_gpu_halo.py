@@ -261,3 +261,89 @@ def test_coupled_pair_past_one_cluster_has_no_exact_fallback():
     with Engine(w) as eng:
         with pytest.raises(NotImplementedError, match="no exact fallback"):
             eng.run_epoch(3)
+
+
+def _two_long_rods():
+    w = wl._world()
+    for z in (0.0, 0.05):
+        w.add_rod(st.init_rod(1025, 2.048, axis=(1.0, 0.0, 0.0), origin=(0.0, 0.0, z)), st.RodParams(**wl.MATERIAL))
+    w.finalize()
+    for r in (0, 1):
+        w.clamp_point(r, 0)
+        w.clamp_frame(r, 0)
+    return w
+
+
+def test_several_halo_groups_bitwise():
+    # two unbound long rods: two cluster groups, two wide-halo launches per epoch
+    g, r = _two_long_rods(), _two_long_rods()
+    with Engine(g) as eng:
+        plan = eng.plan()["groups"]
+        assert len(plan) == 2 and all(x["halo"] for x in plan)
+        for _ in range(6):
+            eng.run_epoch(7)
+    OracleStepper(r).run(42)
+    assert_bitwise(g, r)
+
+
+def test_halo_group_beside_a_batch_of_short_rods_bitwise():
+    # a long rod and 40 short ones: a CTA-tier group (general / one-warp
+    # kernels) and a wide-halo cluster group in one world
+    def make():
+        w = wl._world()
+        w.add_rod(st.init_rod(700, 1.4, axis=(1.0, 0.0, 0.0)), st.RodParams(**wl.MATERIAL))
+        for k in range(40):
+            w.add_rod(st.init_rod(17, 0.032, axis=(0.0, 0.0, 1.0), origin=(0.01 * k, 0.1, 0.0)),
+                      st.RodParams(**wl.MATERIAL))
+        w.finalize()
+        for rr in range(41):
+            w.clamp_point(rr, 0)
+        return w
+    g, r = make(), make()
+    with Engine(g) as eng:
+        plan = eng.plan()["groups"]
+        assert any(x["halo"] for x in plan) and any(not x["halo"] for x in plan)
+        for _ in range(4):
+            eng.run_epoch(10)
+    OracleStepper(r).run(40)
+    assert_bitwise(g, r)
+
+
+def test_mesh_contacts_fp32_within_tolerance():
+    # the insertion scene on the halo kernel in fp32: positions near the
+    # fp64 oracle's after 400 steps (contacts switch on and off along the way)
+    g, r = wl.insertion(), wl.insertion()
+    with Engine(g, precision="f32") as eng:
+        assert eng.plan()["groups"][0]["halo"]
+        eng.run_epoch(400)
+    OracleStepper(r).run(400)
+    # the rod sits ~0.3 m from the origin: fp32 rounding of its driven base
+    # (ulp ~3e-8 m) accumulates over the 400 steps to ~3e-6 m
+    assert np.max(np.abs(g.positions - r.positions)) <= 2e-5
+    assert np.max(np.abs(g.frames - r.frames)) <= 1e-4
+
+
+def test_live_commands_with_mesh_contacts_bitwise():
+    # live launches of the insertion scene (scene-feature path of the halo
+    # kernel): a driver command posted mid-epoch lands at a step boundary
+    import threading
+    import time
+    steps = 4000
+    g = wl.insertion()
+    with Engine(g, live=True) as eng:
+        assert eng.plan()["live"] and eng.plan()["groups"][0]["halo"]
+        eng.run_epoch(1)
+        box = {}
+        th = threading.Thread(target=lambda: box.setdefault("m", eng.run_epoch(steps)))
+        th.start()
+        time.sleep(0.01)
+        t = eng.post_command("insert_velocity", rod=0, value=0.08, axis=(0.0, 0.0, 1.0))
+        th.join()
+        s_apply = t.wait(5.0)
+    assert 1 < s_apply < 1 + steps
+    r = wl.insertion()
+    o = OracleStepper(r)
+    o.run(s_apply)
+    r.driver_velocity[0] = (0.0, 0.0, 0.08)
+    o.run(1 + steps - s_apply)
+    assert_bitwise(g, r)
