@@ -610,11 +610,11 @@ int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std
             int S, G, C, threads, wmax;
             std::vector<HaloTask> ts;
         };
-        auto make_cand = [&](bool cgx) -> Cand {
+        auto make_cand = [&](bool cgx, int s_cap) -> Cand {
             Cand c{};
             c.gx = cgx;
             c.S = h->live ? 1 : h->halo_steps > 0 ? h->halo_steps
-                              : cgx ? std::max(1, std::min(kHaloGridSteps, 96 / R1)) : (R1 == 1 ? 2 : 1);
+                              : cgx ? std::max(1, std::min({kHaloGridSteps, 96 / R1, s_cap})) : (R1 == 1 ? 2 : 1);
             c.G = c.S * R1;
             int C;
             if (!cgx) {
@@ -641,17 +641,23 @@ int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std
             c.threads = (nr * c.wmax + 31) / 32 * 32;
             return c;
         };
+        // the grid candidate: the longest exchange period whose CTAs fit 512 threads
+        auto grid_cand = [&]() -> Cand {
+            Cand gr = make_cand(true, kHaloGridSteps);
+            for (int sc = gr.S - 1; sc >= 1 && gr.threads > 512; --sc) gr = make_cand(true, sc);
+            return gr;
+        };
         std::vector<Cand> cands;
         if (h->halo_grid == 1 && !h->live) {
-            cands.push_back(make_cand(true));
+            cands.push_back(grid_cand());
         } else if (h->halo_grid == 0 || h->live) {
-            cands.push_back(make_cand(false));
+            cands.push_back(make_cand(false, 1));
         } else {
-            Cand cl = make_cand(false);
+            Cand cl = make_cand(false, 1);
             if (cl.threads <= 256) {
                 cands.push_back(cl);
             } else {
-                Cand gr = make_cand(true);
+                Cand gr = grid_cand();
                 if (gr.threads < cl.threads) cands.push_back(gr);   // (thinner CTAs than the cluster's)
                 cands.push_back(cl);
                 cands.push_back(gr);
@@ -2329,7 +2335,19 @@ int rs_update_params(rs_handle h, double dt, int64_t iters) {
     }
     if (dt <= 0.0 || iters < 1) return fail(RS_E_INVALID, "dt must be positive and iters >= 1");
     h->d.dt = dt;
+    const bool more = iters > h->d.iters;
     h->d.iters = iters;
+    // more iterations than a wide-halo group's ghosts cover: plan again (the
+    // ghost width is 2I + 1 points per exchanged step)
+    bool replan = false;
+    if (more && h->planned)
+        for (const Group& g : h->groups)
+            replan = replan || (g.halo && g.h_g != g.h_s && g.h_s * (2 * iters + 1) > g.h_g);
+    if (replan) {
+        CK(cudaSetDevice(h->d.device));
+        CK(cudaStreamSynchronize(h->st));
+        if (int rc = upload_static(h)) return rc;
+    }
     return RS_OK;
 }
 

@@ -196,7 +196,7 @@ def test_error_step_surfaces():
 
 def test_more_iterations_than_the_ghost_width_bitwise():
     # the ghost width covers the planned iteration count; more iterations
-    # run on the general kernel, fewer stay on the halo kernel
+    # plan the halo again (wider ghosts), fewer keep the plan
     g, r = wl.pair(), wl.pair()
     ref = OracleStepper(r)
     with Engine(g) as eng:
@@ -205,6 +205,20 @@ def test_more_iterations_than_the_ghost_width_bitwise():
             ref.set_params(iterations=it)
             eng.run_epoch(steps)
             ref.run(steps)
+            assert eng.plan()["groups"][0]["halo"]["ghost"] >= 2 * it + 1
+    assert_bitwise(g, r)
+
+
+def test_more_iterations_on_coupled_rods_past_one_cluster_bitwise():
+    g, r = wl.pair(9500, 19.0), wl.pair(9500, 19.0)
+    ref = OracleStepper(r)
+    with Engine(g) as eng:
+        eng.run_epoch(3)
+        ref.run(3)
+        eng.set_params(iterations=14)
+        ref.set_params(iterations=14)
+        eng.run_epoch(3)
+        ref.run(3)
     assert_bitwise(g, r)
 
 
