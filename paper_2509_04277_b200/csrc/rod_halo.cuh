@@ -947,6 +947,8 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         }
         __syncthreads();
         any = *vote;
+    } else if (ncl == 1) {   // one CTA: its own vote
+        any = bad;
     } else {
         if (t == 0) *vote = bad;
         cluster_barrier();
