@@ -324,10 +324,8 @@ int ensure_stage(rs_handle h, size_t bytes) {
 }
 
 // host double array -> device Real array
-// Several copies between the World's host arrays and the device as one
-// driver call (cudaMemcpyBatchAsync, stream-ordered sources): a small world's
-// epoch moves a few arrays each way, and one call per array cost more than
-// the copies.
+// Several copies between the World's host arrays and the device, collected
+// and issued back to back on one stream (one cudaMemcpyAsync per array).
 struct CopyBatch {
     void* dst[8];
     void* src[8];
@@ -344,14 +342,8 @@ struct CopyBatch {
 
 int flush_batch(rs_handle h, CopyBatch& b, cudaStream_t st = nullptr) {
     if (!st) st = h->st;
-    if (b.n == 1) {
-        CK(cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, st));
-    } else if (b.n > 1) {
-        cudaMemcpyAttributes attr = {};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        size_t first = 0, fail_idx = 0;
-        CK(cudaMemcpyBatchAsync(b.dst, b.src, b.size, b.n, &attr, &first, 1, &fail_idx, st));
-    }
+    for (size_t i = 0; i < b.n; ++i)
+        CK(cudaMemcpyAsync(b.dst[i], b.src[i], b.size[i], cudaMemcpyDefault, st));
     b.n = 0;
     return RS_OK;
 }
