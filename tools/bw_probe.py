@@ -55,7 +55,10 @@ def main():
     ap.add_argument("--launches", type=int, default=20)
     ap.add_argument("--precision", default="f64")
     ap.add_argument("--shapes", default="3")
+    ap.add_argument("--lib", default=None, help="library build to load (A/B of builds)")
     a = ap.parse_args()
+    if a.lib:
+        _lib._LIB = _lib.load_library(a.lib)
     ref, ms_ref, plan_ref, _ = run(a.rods, a.k, a.launches, a.precision, {"RSB_BW": "0"})
     out = {"rods": a.rods, "k": a.k, "launches": a.launches, "precision": a.precision,
            "general_ms_per_launch": ms_ref}
@@ -71,6 +74,8 @@ def main():
                 diff[s] = float(np.max(np.abs(x - y)))
         out[f"shape{sh}"] = {"ms_per_launch": ms, "diff": diff, "redo_last": redo,
                              "speedup": ms_ref / ms}
+    if a.lib:
+        out["lib"] = os.path.basename(a.lib)
     print(json.dumps(out))
 
 
