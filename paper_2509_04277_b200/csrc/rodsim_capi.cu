@@ -206,6 +206,7 @@ struct rs_handle_s {
     int halo_grid = -1;             // RSB_HALO_GRID: 1 grid exchange, 0 cluster only, -1 the planner's
     int halo_width = 128;           // RSB_HALO_W: target threads per CTA of the grid exchange
     int halo_steps = 0;             // RSB_HALO_STEPS: steps per exchange (0: the planner's)
+    int max_k = kMaxStepsPerLaunch; // RSB_MAX_K: steps per launch cap (launch-cost probes)
     bool halo_pending = false;      // wide-halo launches not yet checked for a failed vote
     bool halo_check_enqueued = false;   // their redo words are on the way to h_hfail
     int64_t* h_hfail = nullptr;     // pinned, one per group
@@ -2078,6 +2079,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     if (const char* e = getenv("RSB_HALO_GRID")) h->halo_grid = atoi(e);
     if (const char* e = getenv("RSB_HALO_W")) h->halo_width = std::max(64, atoi(e));
     if (const char* e = getenv("RSB_HALO_STEPS")) h->halo_steps = std::max(0, atoi(e));
+    if (const char* e = getenv("RSB_MAX_K")) h->max_k = std::max(1, std::min(kMaxStepsPerLaunch, atoi(e)));
     if (const char* e = getenv("RSB_HALO_CTA")) h->halo_cta = atoi(e);
     if (const char* sp = getenv("RSB_BW")) h->bw_on = atoi(sp) != 0;
     if (const char* sp = getenv("RSB_RW")) h->rw_on = atoi(sp) != 0;
@@ -2178,7 +2180,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
     if (h->bar_timing) CK(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned long long), h->st));
     int64_t done = 0;
     while (done < steps) {
-        const int k = int(std::min<int64_t>(steps - done, kMaxStepsPerLaunch));
+        const int k = int(std::min<int64_t>(steps - done, h->max_k));
         if (h->contacts_on || h->d.has_self)
             CK(cudaMemsetAsync(h->d_contacts, 0, sizeof(unsigned long long), h->st));
         for (const Group& g : h->groups) {
