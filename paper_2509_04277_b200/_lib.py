@@ -292,6 +292,12 @@ class DeviceWorld:
         h = _p()
         check(self.lib.rs_create(ctypes.byref(d), ctypes.byref(h)), self.lib)
         self.handle = h
+        # run()'s out-parameters and entry point, made once: a one-step
+        # launch is a few microseconds, and the per-call ctypes objects were
+        # a third of its host time
+        self._contacts, self._bns = _i64(0), _i64(0)
+        self._out = (ctypes.byref(self._contacts), ctypes.byref(self._bns))
+        self._run_epoch = self.lib.rs_run_epoch
 
     def state_pointers(self):
         return tuple(self.arrays[k].ctypes.data for k in ("pos", "vel", "q", "w"))
@@ -300,10 +306,10 @@ class DeviceWorld:
         check(self.lib.rs_upload(self.handle, mask), self.lib)
 
     def run(self, steps):
-        contacts, bns = _i64(0), _i64(0)
-        check(self.lib.rs_run_epoch(self.handle, int(steps), ctypes.byref(contacts),
-                                    ctypes.byref(bns)), self.lib)
-        return contacts.value, bns.value
+        rc = self._run_epoch(self.handle, int(steps), *self._out)
+        if rc != RS_OK:
+            check(rc, self.lib)
+        return self._contacts.value, self._bns.value
 
     def run_host(self, steps):
         """Upload the state, run `steps` steps, download the state (one

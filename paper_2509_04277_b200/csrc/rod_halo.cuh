@@ -128,11 +128,12 @@ __device__ __forceinline__ void hl_div(const R (&a)[N], R b, R rb, bool b_ok, bo
 // (with the code present but idle, cfg4 N = 256 ran 4.2 -> 4.7 us per step).
 template <typename Real, int MODE, bool GEN, bool BIND, int TB, bool GX, bool XF>
 __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // Programmatic dependent launch: the next launch of the stream may be
+    // scheduled at once; this one waits for the previous grid (and its
+    // writes) only after the loads of data no kernel writes -- the plan's
+    // task and offset tables, point flags, masses -- so their round trips
+    // overlap the previous launch's tail (griddepcontrol.wait below).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // an earlier launch of this group failed its vote: the host replays
-    // the exact kernel from that launch's first step, this one does nothing
-    if (*reinterpret_cast<volatile int64_t*>(A.hfail)) return;
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Real* sm = reinterpret_cast<Real*>(smem_raw);
@@ -219,16 +220,7 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     const int t_l = BIND ? 2 * (i - x0_l) + r : r * W + (i - x0_l);
     const int t_r = BIND ? 2 * (i - x0_r) + r : r * W + (i - x0_r);
 
-    // ---- state and statics ----
-    Real p[3], v[3], q[4], w[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        p[k] = A.pos[3 * size_t(pt) + k];
-        v[k] = A.vel[3 * size_t(pt) + k];
-        w[k] = A.w[3 * size_t(el) + k];
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = A.q[4 * size_t(el) + k];
+    // ---- statics (written by host copies only) ----
     const uint32_t fl = A.pflags[pt];
     const bool pl = (fl & SF_PLOCK) != 0, flk = (fl & SF_FLOCK) != 0;
     const bool dist = (fl & SF_DIST) != 0, ext = (fl & SF_EXT) != 0;
@@ -259,6 +251,20 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
         rwsP[c] = a_side[c] ? rws : rws_l;
         actP[c] = (a_side[c] ? act : act_l) && pv;
     }
+    // ---- the previous launch's results from here on ----
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // an earlier launch of this group failed its vote: the host replays
+    // the exact kernel from that launch's first step, this one does nothing
+    if (*reinterpret_cast<volatile int64_t*>(A.hfail)) return;
+    Real p[3], v[3], q[4], w[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        p[k] = A.pos[3 * size_t(pt) + k];
+        v[k] = A.vel[3 * size_t(pt) + k];
+        w[k] = A.w[3 * size_t(el) + k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = A.q[4 * size_t(el) + k];
     // drivers (_core.pyx:866-875): the rod driving this point / this frame
     const int drp = pv ? A.hdrv[2 * pt] : -1, drf = ev ? A.hdrv[2 * pt + 1] : -1;
     Real dvel[3] = {Real(0), Real(0), Real(0)}, drot = Real(0);
