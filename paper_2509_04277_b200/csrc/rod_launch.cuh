@@ -55,6 +55,21 @@ static cudaError_t configure_once(Fn fn, std::atomic<bool>* done) {
     return cudaSuccess;
 }
 
+// clusters of more than 8 CTAs (non-portable sizes): the function attribute
+// is set once per device like the ones above, not before every launch (a
+// driver call that cost K = 1 launches of 16-CTA clusters host time)
+template <typename Fn>
+static cudaError_t allow_wide_clusters(Fn fn, std::atomic<bool>* done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev].store(true, std::memory_order_release);
+    return cudaSuccess;
+}
+
 template <typename Real, int S, int CAP, int TIER, int UNI>
 static std::atomic<bool>* configured_flags() {
     static std::atomic<bool> done[64];
@@ -69,7 +84,8 @@ static cudaError_t launch_one(const StepArgs<Real>& a, int ncta, int threads,
     if (e != cudaSuccess) return e;
     if constexpr (TIER == TIER_CLUSTER) {
         if (cluster > 8) {
-            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            static std::atomic<bool> wide[64];
+            e = allow_wide_clusters(fn, wide);
             if (e != cudaSuccess) return e;
         }
         cudaLaunchConfig_t cfg = {};
@@ -114,7 +130,8 @@ static cudaError_t occupancy_one(int threads, size_t smem, int cluster, int* out
     if (e != cudaSuccess) return e;
     if constexpr (TIER == TIER_CLUSTER) {
         if (cluster > 8) {
-            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            static std::atomic<bool> wide[64];
+            e = allow_wide_clusters(fn, wide);
             if (e != cudaSuccess) return e;
         }
         cudaLaunchConfig_t cfg = {};
@@ -326,7 +343,8 @@ static cudaError_t halo_one(int what, const StepArgs<Real>* a, int ncta, int thr
         return cudaLaunchKernelEx(&cfg, fn, *a);
     }
     if (ncta > 8) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        static std::atomic<bool> wide[64];
+        e = allow_wide_clusters(fn, wide);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
