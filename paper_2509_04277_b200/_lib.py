@@ -274,6 +274,11 @@ def plan_dry(world, num_sms=148, precision="f64", **force):
     return json.loads(buf.value.decode())
 
 
+# rs_run_epoch with plain integer arguments (handle and out-parameter
+# addresses): the cheapest ctypes conversion for one-step launches
+_RUN_PROTO = ctypes.CFUNCTYPE(ctypes.c_int32, _p, _i64, _p, _p)
+
+
 class DeviceWorld:
     """One device mirror of a World (a C handle) plus the arrays it binds.
 
@@ -296,8 +301,9 @@ class DeviceWorld:
         # launch is a few microseconds, and the per-call ctypes objects were
         # a third of its host time
         self._contacts, self._bns = _i64(0), _i64(0)
-        self._out = (ctypes.byref(self._contacts), ctypes.byref(self._bns))
-        self._run_epoch = self.lib.rs_run_epoch
+        self._out = (ctypes.addressof(self._contacts), ctypes.addressof(self._bns))
+        self._hval = h.value
+        self._run_epoch = _RUN_PROTO(("rs_run_epoch", self.lib))
 
     def state_pointers(self):
         return tuple(self.arrays[k].ctypes.data for k in ("pos", "vel", "q", "w"))
@@ -306,7 +312,7 @@ class DeviceWorld:
         check(self.lib.rs_upload(self.handle, mask), self.lib)
 
     def run(self, steps):
-        rc = self._run_epoch(self.handle, int(steps), *self._out)
+        rc = self._run_epoch(self._hval, int(steps), *self._out)
         if rc != RS_OK:
             check(rc, self.lib)
         return self._contacts.value, self._bns.value
@@ -401,6 +407,7 @@ class DeviceWorld:
         if getattr(self, "handle", None):
             self.lib.rs_destroy(self.handle)
             self.handle = None
+            self._hval = None   # run() after close: a null handle (RS_E_INVALID)
 
     def __del__(self):
         try:
