@@ -48,6 +48,10 @@ template <typename Real, int MODE, bool GEN>
 __global__ void __launch_bounds__(32, 1) rod_warp1_kernel(const StepArgs<Real> A) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // lazy single-rod launches (redo_mode 2): an earlier launch failed its
+    // vote and left its first step in the group's redo word; the host
+    // replays the exact kernel from there, this launch does nothing
+    if (A.redo_mode == 2 && *reinterpret_cast<volatile int64_t*>(A.hfail)) return;
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = int(threadIdx.x & 31u);
     const int ti = int(blockIdx.x);
@@ -342,7 +346,10 @@ __global__ void __launch_bounds__(32, 1) rod_warp1_kernel(const StepArgs<Real> A
     }
 
     if (__any_sync(FULL, !ok)) {
-        if (lane == 0) A.redo_list[atomicAdd(A.redo_count, 1)] = ti;
+        if (lane == 0) {
+            if (A.redo_mode == 2) *A.hfail = A.step0 + 1;   // lazy: nothing written back
+            else A.redo_list[atomicAdd(A.redo_count, 1)] = ti;
+        }
         return;
     }
     if (pv) {

@@ -156,6 +156,7 @@ struct Group {       // one kernel launch
     HaloTask* d_htask = nullptr;
     int32_t* d_hflags = nullptr;    // grid exchange: per-CTA flags, arrival count, vote OR
     int64_t* d_hfail = nullptr;     // lazy redo word (StepArgs::hfail)
+    mutable int lazy_skip = 0;      // lazy one-warp launches paused after a replay
     void* d_hhalo = nullptr;        // grid exchange: (2, C, 2, NR, G, 13) halo records
 };
 
@@ -166,7 +167,7 @@ struct Group {       // one kernel launch
 // a 256-element sweep rod redid every launch (6.4 -> 9.9 us/step).
 constexpr int kSpecMinSteps = 32;
 constexpr int kHaloCtaMinPoints = 100;
-constexpr int kHaloCtaShortPoints = 40;
+constexpr int kHaloCtaShortPoints = 2;   // every one-CTA rod (tools/short_probe.py)
 constexpr int kHaloGridSteps = 3;
 constexpr int kSpecBackoff = 64;
 bool spec_group(const Group& g) {
@@ -207,6 +208,8 @@ struct rs_handle_s {
     int halo_width = 128;           // RSB_HALO_W: target threads per CTA of the grid exchange
     int halo_steps = 0;             // RSB_HALO_STEPS: steps per exchange (0: the planner's)
     int max_k = kMaxStepsPerLaunch; // RSB_MAX_K: steps per launch cap (launch-cost probes)
+    int halo_short = kHaloCtaShortPoints;   // RSB_HALO_SHORT: smallest one-CTA rod on the halo kernel
+    bool rw_lazy = true;            // RSB_RW_LAZY=0: one-warp rods only with a consume launch, K >= 32
     bool halo_pending = false;      // wide-halo launches not yet checked for a failed vote
     bool halo_check_enqueued = false;   // their redo words are on the way to h_hfail
     int64_t* h_hfail = nullptr;     // pinned, one per group
@@ -512,11 +515,13 @@ int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std
         // Smaller one-CTA rods (kHaloCtaShortPoints .. kHaloCtaMinPoints)
         // take it as ONE CTA, no ghosts (cfg4, K = 100: 96 points 4.04 ->
         // 3.83 us per step, 64 elements 3.81 -> 3.75; K = 10: 4.23 -> 4.10,
-        // 4.19 -> 3.99); rods the one-warp kernels take (<= 63 elements)
-        // only for epochs shorter than kSpecMinSteps, where those do not run
+        // 4.19 -> 3.99; 2-38 elements, K = 1 / 10: 6.9-7.4 -> 5.8-5.9 /
+        // 4.0-4.2 -> 3.8-3.9); rods the one-warp kernels take (<= 63
+        // elements) only for epochs shorter than kSpecMinSteps, where those
+        // do not run
         const int cta_np = h->h_tasks[g.task_begin].np;
         const bool cta_ok = g.tier == TIER_CTA && g.ncta <= 2 && h->halo_cta != 0 &&
-                            (h->halo_cta == 1 || cta_np >= kHaloCtaShortPoints);
+                            (h->halo_cta == 1 || cta_np >= h->halo_short);
         const bool one_cta = g.tier == TIER_CTA && h->halo_cta != 1 && cta_np < kHaloCtaMinPoints;
         g.h_short = one_cta && g.rw;
         if ((g.tier != TIER_CLUSTER && g.tier != TIER_GRID && !cta_ok) || g.uni != 2 || !h->halo_on ||
@@ -625,7 +630,8 @@ int plan_halo_groups(rs_handle h, const std::vector<uint32_t>& pflags, const std
                 C = h->halo_ctas > 0 ? h->halo_ctas : ctas_for(width);
                 C = std::min(C, h->num_sms > 0 ? h->num_sms : 148);
             }
-            c.C = int(std::min<int64_t>(C, np / c.G));
+            // (one CTA holds the whole rod: no ghosts, any length)
+            c.C = one_cta && !cgx ? 1 : int(std::min<int64_t>(C, np / c.G));
             if (c.C < 1) {
                 c.threads = 1 << 30;
                 return c;
@@ -1684,7 +1690,14 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     // list and returns)
     // (one-CTA rods only for long epochs: the exact launch over the redo
     // list costs a few microseconds, a whole K = 1 step on a short rod)
-    bool spec = !exact && h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
+    // (a single one-warp rod: lazy launches, below)
+    bool lazy_rw = !exact && h->rw_lazy && h->spec && g.rw && g.d_hfail && g.tier == TIER_CTA && g.ncta == 1 &&
+                   t_cnt < 0 && cfg0 < 3 && h->h_grabs.empty() && !h->live;
+    if (lazy_rw && g.lazy_skip > 0) {
+        --g.lazy_skip;
+        lazy_rw = false;
+    }
+    bool spec = !exact && !lazy_rw && h->spec && spec_group(g) && cfg0 < 3 && h->redo_count.p &&
                 (g.tier != TIER_CTA || steps >= kSpecMinSteps);
     const int gi = int(&g - h->groups.data());
     const bool backoff = g.tier == TIER_CTA && gi >= 0 && gi < int(h->groups.size());
@@ -1792,6 +1805,39 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
         auto a = go(make_args<double>(h, g, step0, steps));
         return f64fast::warp_step<double>(gen, g.rw_form, &a, nt, h->st);
     };
+    // A single rod on a one-warp kernel (<= 63 elements) at any epoch length:
+    // launched lazily like the wide-halo kernel -- a failed vote writes
+    // nothing back and leaves the launch's first step in the group's redo
+    // word, later launches return at once, and the host replays the exact
+    // kernel at its next synchronisation -- so no consume launch follows it
+    // (which had kept these kernels off epochs shorter than kSpecMinSteps).
+    // A group that needed a replay runs without speculation for a while.
+    if (lazy_rw) {
+        const int gen = (h->has_fext || g.rw_gen) ? 1 : 0;
+        auto go = [&](auto a) {
+            a.ntasks = 1;
+            a.redo_mode = 2;
+            return a;
+        };
+        cudaError_t el;
+        if (h->prec == RS_F64_MIRROR) {
+            auto a = go(make_args<double>(h, g, step0, steps));
+            el = mirror::warp_step<double>(gen, g.rw_form, &a, 1, h->st);
+        } else if (h->prec == RS_F32) {
+            auto a = go(make_args<float>(h, g, step0, steps));
+            el = f32::warp_step<float>(gen, g.rw_form, &a, 1, h->st);
+        } else {
+            auto a = go(make_args<double>(h, g, step0, steps));
+            el = f64fast::warp_step<double>(gen, g.rw_form, &a, 1, h->st);
+        }
+        if (el != cudaSuccess)
+            return fail(RS_E_CUDA, "one-warp launch failed: %s", cudaGetErrorString(el));
+        h->halo_pending = true;
+        h->last_halo = true;
+        h->last_spec = false;
+        h->launches += 1;
+        return RS_OK;
+    }
     // the wide-halo kernel takes the launch of an eligible group (no grabs,
     // not live, ghost width still covering the iterations); a failed vote is
     // replayed exactly by resolve_halo at the next synchronisation
@@ -1889,6 +1935,7 @@ int finish_halo_check(rs_handle h, bool* replayed) {
         const int64_t v = h->h_hfail[gi];
         if (!g.d_hfail || !v) continue;
         CK(cudaMemsetAsync(g.d_hfail, 0, sizeof(int64_t), h->st));
+        if (g.rw) g.lazy_skip = kSpecBackoff;   // (a rod that fails keeps failing: planar noise)
         const bool lh = h->last_halo;
         for (int64_t s0 = v - 1; s0 < h->step;) {
             const int k = int(std::min<int64_t>(h->step - s0, kMaxStepsPerLaunch));
@@ -2079,6 +2126,8 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     if (const char* e = getenv("RSB_HALO_GRID")) h->halo_grid = atoi(e);
     if (const char* e = getenv("RSB_HALO_W")) h->halo_width = std::max(64, atoi(e));
     if (const char* e = getenv("RSB_HALO_STEPS")) h->halo_steps = std::max(0, atoi(e));
+    if (const char* e = getenv("RSB_RW_LAZY")) h->rw_lazy = atoi(e) != 0;
+    if (const char* e = getenv("RSB_HALO_SHORT")) h->halo_short = std::max(2, atoi(e));
     if (const char* e = getenv("RSB_MAX_K")) h->max_k = std::max(1, std::min(kMaxStepsPerLaunch, atoi(e)));
     if (const char* e = getenv("RSB_HALO_CTA")) h->halo_cta = atoi(e);
     if (const char* sp = getenv("RSB_BW")) h->bw_on = atoi(sp) != 0;

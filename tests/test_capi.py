@@ -208,7 +208,7 @@ def test_plan_barriers_per_step():
 
 
 def test_plan_wide_halo_kernel():
-    # rod_halo.cuh: rods beyond one CTA (and one-CTA rods of >= 100 points)
+    # rod_halo.cuh: rods beyond one CTA (and one-CTA rods: spread over a cluster from 100 points)
     # step with one inter-CTA exchange per step; cluster up to 16 CTAs of <=
     # 256 threads, a co-resident grid beyond; the cfg1 cantilever, forced
     # layouts and overlapping couplings keep the general kernel
@@ -223,7 +223,8 @@ def test_plan_wide_halo_kernel():
     assert halo(wl.sweep(256))["exchange"] == "cluster"
     assert halo(wl.cantilever())["ctas"] == 1                   # one CTA, no ghosts (65 points)
     assert halo(wl.sweep(48))["short_epochs_only"]             # the one-warp kernel for K >= 32
-    assert halo(wl.sweep(16)) is None
+    h16 = halo(wl.sweep(16))                                   # every one-CTA rod, K < 32 only
+    assert h16["ctas"] == 1 and h16["short_epochs_only"]
     assert halo(wl.sweep(1024), force_tier=1, force_ctas=4) is None
     assert halo(wl.hair(2048)) is None
     w = wl.pair()

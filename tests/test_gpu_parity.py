@@ -539,6 +539,35 @@ def test_speculative_single_rod_redo():
         assert dev.last_redo_count() == 0
 
 
+@pytest.mark.parametrize("k", [1, 10, 40])
+@pytest.mark.parametrize("tiny", [False, True])
+def test_lazy_one_warp_rod_bitwise(k, tiny):
+    # a single rod of <= 63 elements steps on a one-warp kernel at any epoch
+    # length, one launch per epoch: a failed vote (tiny: dividends below the
+    # fast path's window) writes nothing back, later launches return at
+    # once, and the download replays the exact kernel from the failed step;
+    # after a replay the rod runs unspeculated for a while -- bitwise either way
+    from paper_2509_04277_b200 import _lib
+    make = (lambda: _tiny_world(1, 16)) if tiny else (lambda: wl.sweep(16))
+    g, r = make(), make()
+    n = 120 // k
+    with Engine(g) as eng:
+        dev = eng.device_world
+        l0 = dev.launch_count()
+        for _ in range(n):
+            dev.run(k)
+        if not tiny:
+            assert dev.launch_count() - l0 == n   # no consume launch behind each
+        dev.download(_lib.RS_STATE)
+        if tiny:
+            assert dev.last_redo_count() in (0, 1)
+        for _ in range(n):                         # after the replay (backoff)
+            dev.run(k)
+        dev.download(_lib.RS_STATE)
+    OracleStepper(r).run(2 * n * k)
+    assert_bitwise(g, r)
+
+
 # -- barrier wait accounting (epoch_results' barrier sum, _core.pyx:1133-1139) --
 
 @pytest.mark.parametrize("make,k", [(wl.pair, 10), (lambda: wl.hair(40), 20),

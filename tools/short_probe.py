@@ -1,7 +1,7 @@
 #!/usr/bin/env python
-"""Short one-CTA rods at K = 1 / 10: the general CTA kernel vs the wide-halo
-kernel as one CTA (RSB_HALO_CTA=1); us/step and whether the two final
-states are bit-identical."""
+"""Short one-CTA rods: default plan vs one env switch (argv: VAR VALUE sizes
+ks; default RSB_HALO_SHORT=2, the wide-halo kernel as one CTA for every
+size); us/step and whether the two final states are bit-identical."""
 import json
 import os
 import sys
@@ -13,12 +13,18 @@ from paper_2509_04277_b200 import workloads as wl  # noqa: E402
 from paper_2509_04277_b200.engine import Engine  # noqa: E402
 
 
+VAR = sys.argv[1] if len(sys.argv) > 1 else "RSB_HALO_SHORT"
+VAL = sys.argv[2] if len(sys.argv) > 2 else "2"
+SIZES = tuple(int(x) for x in sys.argv[3].split(",")) if len(sys.argv) > 3 else (2, 4, 8, 12, 16, 20, 24, 32, 38)
+KS = tuple(int(x) for x in sys.argv[4].split(",")) if len(sys.argv) > 4 else (1, 10)
+
+
 def run(n, k, launches, env):
-    old = os.environ.get("RSB_HALO_CTA")
+    old = os.environ.get(VAR)
     if env is None:
-        os.environ.pop("RSB_HALO_CTA", None)
+        os.environ.pop(VAR, None)
     else:
-        os.environ["RSB_HALO_CTA"] = env
+        os.environ[VAR] = env
     try:
         w = wl.sweep(n)
         with Engine(w) as eng:
@@ -35,17 +41,17 @@ def run(n, k, launches, env):
         return w, round(us, 3), halo
     finally:
         if old is None:
-            os.environ.pop("RSB_HALO_CTA", None)
+            os.environ.pop(VAR, None)
         else:
-            os.environ["RSB_HALO_CTA"] = old
+            os.environ[VAR] = old
 
 
-for n in (8, 16, 24, 32, 38, 48, 63):
-    for k in (1, 10):
+for n in SIZES:
+    for k in KS:
         launches = 2000 // k
         a, ua, ha = run(n, k, launches, None)
-        b, ub, hb = run(n, k, launches, "1")
+        b, ub, hb = run(n, k, launches, VAL)
         same = all(np.array_equal(getattr(a, f).view(np.int64), getattr(b, f).view(np.int64))
                    for f in ("positions", "velocities", "frames", "angular_velocities"))
-        print(json.dumps({"n": n, "k": k, "default_us": ua, "default_halo": ha, "halo_us": ub,
+        print(json.dumps({"n": n, "k": k, "default_us": ua, "default_halo": ha, VAR + "=" + VAL: ub,
                           "halo_planned": hb, "bitwise_equal": same}), flush=True)
