@@ -15,7 +15,7 @@ if len(sys.argv) > 1:   # A/B of library builds (same ABI)
     _lib._LIB = _lib.load_library(sys.argv[1])
     print(os.path.basename(sys.argv[1]), flush=True)
 n = 2000
-for name, mk in (("n16", lambda: wl.sweep(16)), ("cfg1", wl.cantilever), ("n1024", lambda: wl.sweep(1024)),
+for name, mk in (("n16", lambda: wl.sweep(16)), ("n48", lambda: wl.sweep(48)), ("cfg1", wl.cantilever), ("n1024", lambda: wl.sweep(1024)),
                  ("pair", wl.pair)):
     row = {}
     for mode in ("py", "c"):
