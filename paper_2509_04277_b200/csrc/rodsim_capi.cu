@@ -2201,9 +2201,17 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     return RS_OK;
 }
 
+// the handle's device current on this thread (cudaSetDevice only when it
+// is not: every entry point calls this, one-step launches included)
+static cudaError_t use_device(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur == dev) return cudaSuccess;
+    return cudaSetDevice(dev);
+}
+
 int rs_upload(rs_handle h, uint32_t mask) {
     if (!h) return fail(RS_E_INVALID, "null handle");
-    CK(cudaSetDevice(h->d.device));
+    CK(use_device(h->d.device));
     if (int rc = resolve_halo(h)) return rc;
     int rc = RS_OK;
     if (mask & RS_CONTROL) {
@@ -2222,7 +2230,7 @@ int rs_upload(rs_handle h, uint32_t mask) {
 int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
-    CK(cudaSetDevice(h->d.device));
+    CK(use_device(h->d.device));
     int rc = epoch_prelude(h);
     if (rc) return rc;
     if (h->timing) CK(cudaEventRecord(h->ev0, h->st));
@@ -2245,7 +2253,7 @@ int rs_run_epoch(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier
 
 int rs_synchronize(rs_handle h) {
     if (!h) return fail(RS_E_INVALID, "null handle");
-    CK(cudaSetDevice(h->d.device));
+    CK(use_device(h->d.device));
     if (int rc = resolve_halo(h)) return rc;
     if (h->err_pending) {
         CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
@@ -2288,7 +2296,7 @@ int download_control(rs_handle h) {
 
 int rs_download(rs_handle h, uint32_t mask) {
     if (!h) return fail(RS_E_INVALID, "null handle");
-    CK(cudaSetDevice(h->d.device));
+    CK(use_device(h->d.device));
     // the redo words travel with the state; a replay (rare) downloads again
     if (int rc = enqueue_halo_check(h)) return rc;
     const rs_world_desc& d = h->d;
@@ -2343,7 +2351,7 @@ int rs_download(rs_handle h, uint32_t mask) {
 int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barrier_ns) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     if (steps < 1) return fail(RS_E_INVALID, "steps must be >= 1");
-    CK(cudaSetDevice(h->d.device));
+    CK(use_device(h->d.device));
     if (int rc = resolve_halo(h)) return rc;
     const bool pipelined = h->rsz == sizeof(double) && h->groups.size() == 1 && !h->contacts_on &&
                            !h->d.has_mesh && !h->d.has_self &&
@@ -2373,7 +2381,7 @@ int64_t rs_step_counter(rs_handle h) { return h ? h->step : -1; }
 int rs_update_params(rs_handle h, double dt, int64_t iters) {
     if (!h) return fail(RS_E_INVALID, "null handle");
     if (h->halo_pending) {   // a replay runs with the parameters of its steps
-        CK(cudaSetDevice(h->d.device));
+        CK(use_device(h->d.device));
         if (int rc = resolve_halo(h)) return rc;
     }
     if (dt <= 0.0 || iters < 1) return fail(RS_E_INVALID, "dt must be positive and iters >= 1");
@@ -2387,7 +2395,7 @@ int rs_update_params(rs_handle h, double dt, int64_t iters) {
         for (const Group& g : h->groups)
             replan = replan || (g.halo && g.h_g != g.h_s && g.h_s * (2 * iters + 1) > g.h_g);
     if (replan) {
-        CK(cudaSetDevice(h->d.device));
+        CK(use_device(h->d.device));
         CK(cudaStreamSynchronize(h->st));
         if (int rc = upload_static(h)) return rc;
     }
@@ -2396,7 +2404,7 @@ int rs_update_params(rs_handle h, double dt, int64_t iters) {
 
 int rs_barrier_timing(rs_handle h, int on) {
     if (!h) return fail(RS_E_INVALID, "null handle");
-    CK(cudaSetDevice(h->d.device));
+    CK(use_device(h->d.device));
     if (on && !h->d_bar) {
         CK(cudaMalloc(&h->d_bar, sizeof(unsigned long long)));
         CK(cudaMallocHost(&h->h_bar, sizeof(unsigned long long)));
@@ -2477,7 +2485,7 @@ int rs_read_snapshot(rs_handle h, double* pos, double* q, int64_t* seq, int64_t*
 
 void rs_destroy(rs_handle h) {
     if (!h) return;
-    cudaSetDevice(h->d.device);
+    use_device(h->d.device);
     if (h->st) cudaStreamSynchronize(h->st);
     for (DevBuf* b : {&h->pos, &h->vel, &h->q, &h->w, &h->rest, &h->ustar, &h->inert, &h->ks, &h->kp, &h->gt,
                       &h->gr, &h->kb, &h->mass, &h->invm, &h->fext, &h->drv_v, &h->drv_rot, &h->pflags,
@@ -2559,11 +2567,11 @@ int64_t rs_launch_count(rs_handle h) { return h ? h->launches : -1; }
 int64_t rs_last_redo_count(rs_handle h) {
     if (!h) return -1;
     if (h->last_halo) {   // wide-halo groups replayed exactly at the last check
-        if (cudaSetDevice(h->d.device) != cudaSuccess || resolve_halo(h) != RS_OK) return -1;
+        if (use_device(h->d.device) != cudaSuccess || resolve_halo(h) != RS_OK) return -1;
         return h->halo_redone;
     }
     if (!h->redo_count.p || !h->last_spec) return 0;   // the last launch did not speculate
-    if (cudaSetDevice(h->d.device) != cudaSuccess) return -1;
+    if (use_device(h->d.device) != cudaSuccess) return -1;
     int32_t n = 0;
     if (cudaMemcpyAsync(&n, h->redo_count.p, sizeof(n), cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||
         cudaStreamSynchronize(h->st) != cudaSuccess)
@@ -2671,7 +2679,7 @@ int rs_plan_dry(const rs_world_desc* desc, int32_t num_sms, char* buf, int64_t l
 int rs_device_ptr(rs_handle h, int32_t which, void** out) {
     if (!h || !out) return fail(RS_E_INVALID, "null argument");
     if (h->halo_pending) {   // the buffers must hold every launched step
-        CK(cudaSetDevice(h->d.device));
+        CK(use_device(h->d.device));
         if (int rc = resolve_halo(h)) return rc;
     }
     const DevBuf* b[] = {&h->pos, &h->vel, &h->q, &h->w};
