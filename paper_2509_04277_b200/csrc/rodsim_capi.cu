@@ -210,6 +210,7 @@ struct rs_handle_s {
     int max_k = kMaxStepsPerLaunch; // RSB_MAX_K: steps per launch cap (launch-cost probes)
     int halo_short = kHaloCtaShortPoints;   // RSB_HALO_SHORT: smallest one-CTA rod on the halo kernel
     bool rw_lazy = true;            // RSB_RW_LAZY=0: one-warp rods only with a consume launch, K >= 32
+    int pipe_chunks = 16;           // RSB_PIPE_CHUNKS: chunks of a pipelined host epoch
     bool halo_pending = false;      // wide-halo launches not yet checked for a failed vote
     bool halo_check_enqueued = false;   // their redo words are on the way to h_hfail
     int64_t* h_hfail = nullptr;     // pinned, one per group
@@ -2014,7 +2015,6 @@ int epoch_epilogue(rs_handle h, int64_t steps, int64_t* contacts, int64_t* barri
     return RS_OK;
 }
 
-constexpr int kPipeChunks = 16;
 
 // One epoch with the state coming from and going back to the host arrays,
 // the copies of chunk c+1 (H2D) and c-1 (D2H) overlapping the launch on
@@ -2030,7 +2030,7 @@ int run_epoch_pipelined(rs_handle h, int64_t steps, int64_t* contacts, int64_t* 
     // the first chunk alone) and drain (D2H of the last alone) are short
     std::vector<double> w;
     for (double f : {0.125, 0.25, 0.5}) w.push_back(f);
-    for (int i = 0; i < kPipeChunks - 6; ++i) w.push_back(1.0);
+    for (int i = 0; i < h->pipe_chunks - 6; ++i) w.push_back(1.0);
     for (double f : {0.5, 0.25, 0.125}) w.push_back(f);
     double wsum = 0;
     for (double x : w) wsum += x;
@@ -2126,6 +2126,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     if (const char* e = getenv("RSB_HALO_GRID")) h->halo_grid = atoi(e);
     if (const char* e = getenv("RSB_HALO_W")) h->halo_width = std::max(64, atoi(e));
     if (const char* e = getenv("RSB_HALO_STEPS")) h->halo_steps = std::max(0, atoi(e));
+    if (const char* e = getenv("RSB_PIPE_CHUNKS")) h->pipe_chunks = std::max(7, std::min(256, atoi(e)));
     if (const char* e = getenv("RSB_RW_LAZY")) h->rw_lazy = atoi(e) != 0;
     if (const char* e = getenv("RSB_HALO_SHORT")) h->halo_short = std::max(2, atoi(e));
     if (const char* e = getenv("RSB_MAX_K")) h->max_k = std::max(1, std::min(kMaxStepsPerLaunch, atoi(e)));
