@@ -298,6 +298,8 @@ struct rs_handle_s {
     void* stage = nullptr;
     size_t stage_bytes = 0;
     std::vector<void*> registered;
+    double* map_state[4] = {nullptr, nullptr, nullptr, nullptr};   // device aliases of pos, vel, q, w
+    bool xfer_on = true;            // RSB_XFER=0: small worlds' host epochs through copy commands
 };
 
 namespace {
@@ -1959,12 +1961,97 @@ int resolve_halo(rs_handle h) {
     return finish_halo_check(h, nullptr);
 }
 
-void register_host(rs_handle h, void* p, size_t bytes) {
-    if (!p || bytes == 0) return;   // page-locked: async copies, no staging
-    if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess)
-        h->registered.push_back(p);
-    else
+// page-locked (async copies, no staging) and mapped: the device alias lets
+// one kernel move a small world's state (xfer_kernel) instead of a copy
+// command per array
+double* register_host(rs_handle h, void* p, size_t bytes) {
+    if (!p || bytes == 0) return nullptr;
+    if (cudaHostRegister(p, bytes, cudaHostRegisterMapped) != cudaSuccess) {
         cudaGetLastError();
+        return nullptr;
+    }
+    h->registered.push_back(p);
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, p, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return static_cast<double*>(dp);
+}
+
+// A small world's state between the World's mapped host arrays and the
+// device mirrors in one launch (and, device -> host, the error stamp and the
+// groups' redo words into pinned memory, so the host epoch needs a single
+// synchronisation).
+struct XferArgs {
+    const double* src[4];
+    double* dst[4];
+    int64_t n[4];
+    const unsigned long long* wsrc[5];
+    unsigned long long* wdst[5];
+    int nw;
+};
+__global__ void xfer_kernel(const XferArgs x) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+        for (int64_t i = t0; i < x.n[a]; i += stride) x.dst[a][i] = x.src[a][i];
+    if (t0 < x.nw) *x.wdst[t0] = *x.wsrc[t0];
+}
+
+// whether a host epoch of this world can move its state with xfer_kernel
+bool xfer_ok(rs_handle h) {
+    if (!h->xfer_on || h->rsz != sizeof(double) || h->d.has_self || h->contacts_on || h->live) return false;
+    for (double* m : h->map_state)
+        if (!m) return false;
+    const size_t bytes = 8 * (6 * size_t(h->d.P) + 7 * size_t(h->d.E));
+    return bytes <= (size_t(8) << 20) && h->groups.size() <= 4;
+}
+
+int launch_xfer(rs_handle h, bool up) {
+    const rs_world_desc& d = h->d;
+    XferArgs x{};
+    double* dev[4] = {static_cast<double*>(h->pos.p), static_cast<double*>(h->vel.p), static_cast<double*>(h->q.p),
+                      static_cast<double*>(h->w.p)};
+    const int64_t n[4] = {3 * d.P, 3 * d.P, 4 * d.E, 3 * d.E};
+    int64_t tot = 0;
+    for (int a = 0; a < 4; ++a) {
+        x.src[a] = up ? h->map_state[a] : dev[a];
+        x.dst[a] = up ? dev[a] : h->map_state[a];
+        x.n[a] = n[a];
+        tot += n[a];
+    }
+    if (!up) {   // the error stamp and the groups' redo words ride along
+        void* he = nullptr;
+        CK(cudaHostGetDevicePointer(&he, h->h_err, 0));
+        x.wsrc[x.nw] = h->d_err;
+        x.wdst[x.nw++] = static_cast<unsigned long long*>(he);
+        if (h->halo_pending) {
+            const size_t ng = h->groups.size();
+            if (h->h_hfail_n < ng) {
+                if (h->h_hfail) cudaFreeHost(h->h_hfail);
+                h->h_hfail = nullptr;
+                CK(cudaMallocHost(&h->h_hfail, sizeof(int64_t) * ng));
+                h->h_hfail_n = ng;
+            }
+            void* hf = nullptr;
+            CK(cudaHostGetDevicePointer(&hf, h->h_hfail, 0));
+            for (size_t gi = 0; gi < ng; ++gi) {
+                h->h_hfail[gi] = 0;
+                if (!h->groups[gi].d_hfail) continue;
+                x.wsrc[x.nw] = reinterpret_cast<const unsigned long long*>(h->groups[gi].d_hfail);
+                x.wdst[x.nw++] = reinterpret_cast<unsigned long long*>(static_cast<int64_t*>(hf) + gi);
+            }
+            h->halo_check_enqueued = true;
+        }
+    }
+    const int threads = 256;
+    const int grid = int(std::min<int64_t>(std::max<int64_t>((tot + threads * 4 - 1) / (threads * 4), 1),
+                                           std::max(h->num_sms, 1)));
+    xfer_kernel<<<grid, threads, 0, h->st>>>(x);
+    CK(cudaGetLastError());
+    return RS_OK;
 }
 
 }  // namespace
@@ -2126,6 +2213,7 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
     if (const char* e = getenv("RSB_HALO_GRID")) h->halo_grid = atoi(e);
     if (const char* e = getenv("RSB_HALO_W")) h->halo_width = std::max(64, atoi(e));
     if (const char* e = getenv("RSB_HALO_STEPS")) h->halo_steps = std::max(0, atoi(e));
+    if (const char* e = getenv("RSB_XFER")) h->xfer_on = atoi(e) != 0;
     if (const char* e = getenv("RSB_PIPE_CHUNKS")) h->pipe_chunks = std::max(7, std::min(256, atoi(e)));
     if (const char* e = getenv("RSB_RW_LAZY")) h->rw_lazy = atoi(e) != 0;
     if (const char* e = getenv("RSB_HALO_SHORT")) h->halo_short = std::max(2, atoi(e));
@@ -2187,10 +2275,10 @@ int rs_create(const rs_world_desc* desc, rs_handle* out) {
                            cudaMemset(h->d_prof, 0, PROF_SLOTS * sizeof(unsigned long long)) != cudaSuccess))
         return bail(fail(RS_E_CUDA, "profile buffer allocation failed"));
     if (h->rsz == sizeof(double)) {
-        register_host(h, h->d.pos, 3 * sizeof(double) * size_t(h->d.P));
-        register_host(h, h->d.vel, 3 * sizeof(double) * size_t(h->d.P));
-        register_host(h, h->d.q, 4 * sizeof(double) * size_t(h->d.E));
-        register_host(h, h->d.w, 3 * sizeof(double) * size_t(h->d.E));
+        h->map_state[0] = register_host(h, h->d.pos, 3 * sizeof(double) * size_t(h->d.P));
+        h->map_state[1] = register_host(h, h->d.vel, 3 * sizeof(double) * size_t(h->d.P));
+        h->map_state[2] = register_host(h, h->d.q, 4 * sizeof(double) * size_t(h->d.E));
+        h->map_state[3] = register_host(h, h->d.w, 3 * sizeof(double) * size_t(h->d.E));
     }
     if ((rc = upload_control(h))) return bail(rc);
     if ((rc = upload_static(h))) return bail(rc);
@@ -2359,6 +2447,29 @@ int rs_run_epoch_host(rs_handle h, int64_t steps, int64_t* contacts, int64_t* ba
                            (h->groups[0].tier == TIER_CTA || h->groups[0].tier == TIER_STREAM) &&
                            h->groups[0].ncta >= 2 && steps <= kMaxStepsPerLaunch &&
                            !(h->groups[0].halo && h->halo_on);   // (a wide-halo launch covers the group)
+    if (!pipelined && xfer_ok(h)) {
+        // small worlds: state in and out by one kernel each, one synchronisation
+        int rc = launch_xfer(h, true);
+        if (rc) return rc;
+        if ((rc = rs_run_epoch(h, steps, contacts, barrier_ns))) return rc;
+        if ((rc = launch_xfer(h, false))) return rc;
+        h->err_pending = false;   // (the stamp came back with the state)
+        CK(cudaStreamSynchronize(h->st));
+        bool replayed = false;
+        if ((rc = finish_halo_check(h, &replayed))) return rc;
+        if (replayed) {   // exact replay: its error stamp and the state again
+            h->err_pending = true;
+            return rs_download(h, RS_STATE);
+        }
+        if (*h->h_err) h->err_step = std::max<int64_t>(h->err_step, int64_t(*h->h_err) - 1);
+        if (h->timed) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+            h->last_ms = ms;
+            h->timed = false;
+        }
+        return RS_OK;
+    }
     if (!pipelined) {
         int rc = upload_state(h);
         if (rc) return rc;
