@@ -8,7 +8,12 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
+from paper_2509_04277_b200 import _lib  # noqa: E402
 from paper_2509_04277_b200 import workloads as wl  # noqa: E402
+
+if len(sys.argv) > 1:   # A/B of library builds (same ABI)
+    _lib._LIB = _lib.load_library(sys.argv[1])
+    print(os.path.basename(sys.argv[1]), end=" ")
 from paper_2509_04277_b200.engine import Engine  # noqa: E402
 
 w = wl.pair()

@@ -1,0 +1,1 @@
+for r in 1 2 3; do for v in A B; do timeout 300 python tools/haptic_ab.py scratch/lib_$v.so 2>&1 | tail -1; done; done
