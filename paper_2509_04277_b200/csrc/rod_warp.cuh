@@ -29,7 +29,12 @@
 // batched kernel (rod_batch.cuh).  Speculative only: a rod whose operand
 // checks fail is left to the exact CTA kernel (redo list).  The planner
 // routes single-rod CTA-tier tasks here (launch-uniform material, no
-// drivers, bindings, grabs, contacts) for epochs of >= kSpecMinSteps steps.
+// drivers, bindings, grabs, contacts).  A world of one such rod launches
+// lazily at any epoch length (redo_mode 2): a failed vote writes nothing
+// back and stamps the group's redo word, later launches return at once,
+// and the host replays the exact kernel at its next synchronisation; a
+// batch of them keeps the redo list and its consume launch (epochs of >=
+// kSpecMinSteps steps).
 #pragma once
 
 #include "rod_warp1.cuh"

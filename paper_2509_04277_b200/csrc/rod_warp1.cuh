@@ -20,7 +20,8 @@
 // and one dependency chain.
 //
 // Arithmetic as in rod_batch.cuh / rod_warp.cuh (the reference's expression
-// order); speculative only, exact CTA kernel over the redo list otherwise.
+// order); speculative only, exact CTA kernel over the redo list otherwise
+// (a single rod: lazily, through the group's redo word -- rod_warp.cuh).
 #pragma once
 
 #include "rod_batch.cuh"
