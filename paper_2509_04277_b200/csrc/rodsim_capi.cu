@@ -1967,7 +1967,11 @@ int resolve_halo(rs_handle h) {
 double* register_host(rs_handle h, void* p, size_t bytes) {
     if (!p || bytes == 0) return nullptr;
     if (cudaHostRegister(p, bytes, cudaHostRegisterMapped) != cudaSuccess) {
-        cudaGetLastError();
+        cudaGetLastError();   // (page-locked without the mapping: copy commands only)
+        if (cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess)
+            h->registered.push_back(p);
+        else
+            cudaGetLastError();
         return nullptr;
     }
     h->registered.push_back(p);
