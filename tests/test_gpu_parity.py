@@ -568,6 +568,22 @@ def test_lazy_one_warp_rod_bitwise(k, tiny):
     assert_bitwise(g, r)
 
 
+@pytest.mark.parametrize("make", [wl.cantilever, wl.pair, lambda: wl.sweep(16)])
+@pytest.mark.parametrize("xfer", ["1", "0"])
+def test_small_world_host_epochs_bitwise(make, xfer, monkeypatch):
+    # Engine.run_epoch on a small world moves the state through the mapped
+    # World arrays with one kernel each way (RSB_XFER=0: copy commands);
+    # either way the host arrays after every epoch equal the oracle's
+    monkeypatch.setenv("RSB_XFER", xfer)
+    g, r = make(), make()
+    ref = OracleStepper(r)
+    with Engine(g) as eng:
+        for k in (1, 7, 10, 33):
+            eng.run_epoch(k)
+            ref.run(k)
+            assert_bitwise(g, r)
+
+
 # -- barrier wait accounting (epoch_results' barrier sum, _core.pyx:1133-1139) --
 
 @pytest.mark.parametrize("make,k", [(wl.pair, 10), (lambda: wl.hair(40), 20),
