@@ -1685,7 +1685,7 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
                  bool exact = false) {
     if (g.tier == TIER_GRID) CK(cudaMemsetAsync(g.d_flags, 0, sizeof(int32_t) * g.ncta, h->st));
     const int nt = t_cnt < 0 ? g.ncta : t_cnt;
-    const int grid = t_cnt < 0 ? g.grid : (g.tier == TIER_STREAM ? std::min(g.grid, nt) : nt);
+    const int grid_full = t_cnt < 0 ? g.grid : (g.tier == TIER_STREAM ? std::min(g.grid, nt) : nt);
     const int cfg0 = launch_cfg(h, g);
     // batched rods (stream tier, variant 7): a speculative launch whose
     // quotients never take the IEEE fallback, then the exact kernel over the
@@ -1734,6 +1734,10 @@ int launch_group(rs_handle h, const Group& g, int64_t step0, int steps, int t_of
     h->last_spec = spec;
     if (spec) CK(cudaMemsetAsync(h->redo_count.p, 0, sizeof(int32_t), h->st));
     auto one = [&](int cfg, int redo_mode) -> cudaError_t {
+        // the stream tier's consume launch walks the redo list (almost
+        // always empty) with one CTA per SM, not the full persistent grid
+        const int grid = (redo_mode == 1 && g.tier == TIER_STREAM) ? std::min(grid_full, std::max(h->num_sms, 1))
+                                                                    : grid_full;
         auto finish = [&](auto& a) {
             a.tasks += t_off;
             a.ntasks = nt;
