@@ -256,6 +256,12 @@ __global__ void __launch_bounds__(TB, 1) rod_halo_kernel(const StepArgs<Real> A)
     // an earlier launch of this group failed its vote: the host replays
     // the exact kernel from that launch's first step, this one does nothing
     if (*reinterpret_cast<volatile int64_t*>(A.hfail)) return;
+    if (A.debug & 1) {   // poison shared memory: uninitialised reads become NaN
+        const size_t words = halo_smem_bytes(T, sizeof(Real)) / 4;
+        for (size_t x = size_t(t); x < words; x += size_t(T)) reinterpret_cast<uint32_t*>(smem_raw)[x] = 0xffffffffu;
+        if (!GX && ncl > 1) cluster_barrier();   // (before any neighbour's DSMEM store)
+        else __syncthreads();
+    }
     Real p[3], v[3], q[4], w[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
